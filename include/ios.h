@@ -1,0 +1,195 @@
+/* ios.h — C-ABI of the B200-native IOS stage executor (arXiv 2011.01302).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n.
+ *
+ * The library implements the paper's problem statement (Sec. 3) and Algorithm 1
+ * with a B200 execution engine:
+ *   ios_graph_create / ios_add_op   build G = (V, E); edges are tensors
+ *   ios_stage_latency               GenerateStage's measurement of one stage (S', T) (Alg. 1 L25/L27)
+ *   ios_schedule_dp                 InterOperatorScheduler with pruning P(r, s) per block
+ *   ios_run                         executes Q stage by stage
+ *
+ * Conventions (all functions):
+ *   - Every call returns ios_status; IOS_OK = 0. No C++ exception crosses the ABI.
+ *   - Out-parameters are written only on IOS_OK. ios_last_error() returns a thread-local message
+ *     describing the last failure on the calling thread (valid until the next call on that thread).
+ *   - Ownership: the library COPIES every host array passed in (weights, biases, add weights,
+ *     schedule arrays) and owns every device buffer it allocates, except the caller's I/O
+ *     pointers of ios_run / ios_op_output, which stay caller-owned.
+ *   - Threading: a graph is single-owner; calls on one handle are not re-entrant. Different
+ *     graphs (e.g. one per GPU) are independent.
+ *   - Device memory is touched lazily: graph construction and ios_schedule_dp with a cost
+ *     callback never initialise CUDA, so they run on machines without a GPU.
+ *   - There is no CPU fallback: without a usable sm_100 device, device calls return IOS_ERR_CUDA.
+ */
+#ifndef IOS_H_
+#define IOS_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define IOS_API __attribute__((visibility("default")))
+#else
+#define IOS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ios_graph_s* ios_graph;       /* opaque; library-owned; free with ios_graph_destroy */
+typedef struct ios_schedule_s* ios_schedule; /* opaque; library-owned; free with ios_schedule_destroy */
+
+typedef enum {
+  IOS_OK = 0,
+  IOS_ERR_INVALID_ARG = 1,
+  IOS_ERR_DANGLING_INPUT = 2, /* an input id does not name an existing op */
+  IOS_ERR_SHAPE = 3,          /* shapes of the inputs are inconsistent with the op */
+  IOS_ERR_BLOCK = 4,          /* edge from a later block, non-contiguous block, or > 64 ops in a block */
+  IOS_ERR_NOT_MERGEABLE = 5,  /* operator merge requested for a set that cannot be merged */
+  IOS_ERR_NOT_A_STAGE = 6,    /* ops not in one block, repeated, or not a valid stage */
+  IOS_ERR_BAD_SCHEDULE = 7,   /* Q is not a valid sequence of endings */
+  IOS_ERR_CUDA = 8,           /* CUDA runtime error or no usable sm_100 device */
+  IOS_ERR_OOM = 9,
+  IOS_ERR_KERNEL = 10,        /* in-kernel dependency wait timed out (deadlock guard) */
+  IOS_ERR_UNSUPPORTED = 11    /* valid request the engine does not implement */
+} ios_status;
+
+typedef enum {
+  IOS_MATH_TF32 = 0,      /* fp32 storage, tcgen05 kind::tf32 operands, fp32 accumulation */
+  IOS_MATH_BF16 = 1,      /* bf16 storage, tcgen05 kind::f16 (bf16) operands, fp32 accumulation */
+  IOS_MATH_FP32_SIMT = 2  /* fp32 storage, CUDA-core fp32 FMA (reference-precision path) */
+} ios_math;
+
+typedef enum { IOS_CONCURRENT = 0, IOS_MERGE = 1 } ios_strategy;   /* T_i */
+
+typedef enum {             /* which strategies GenerateStage may use (Fig. 6) */
+  IOS_BOTH = 0,            /* IOS-Both (the paper's IOS)                                 */
+  IOS_MERGE_ONLY = 1,      /* IOS-Merge: multi-op stages must be merged                  */
+  IOS_PARALLEL_ONLY = 2    /* IOS-Parallel: concurrent execution only                    */
+} ios_strategy_set;
+
+typedef enum {
+  IOS_OP_CONV = 0,           /* Conv(-ReLU) unit: 1 input                                     */
+  IOS_OP_SEPCONV = 1,        /* Relu-SepConv unit: n inputs summed with add_weights, ReLU,
+                                depthwise kernel_h x kernel_w (stride, pad), pointwise to out_channels  */
+  IOS_OP_MAXPOOL = 2,        /* 1 input, window kernel_h x kernel_w                                   */
+  IOS_OP_AVGPOOL = 3,        /* 1 input; IOS_F_COUNT_INCLUDE_PAD selects the divisor                   */
+  IOS_OP_GLOBAL_AVGPOOL = 4, /* 1 input -> [N, C, 1, 1]                                               */
+  IOS_OP_ADD = 5,            /* n inputs of equal shape: sum_i add_weights[i] * x_i                   */
+  IOS_OP_CONCAT = 6,         /* n inputs, concatenated along C in order                       */
+  IOS_OP_IDENTITY = 7,       /* 1 input, copied                                                        */
+  IOS_OP_LINEAR = 8          /* FC head: 1 input of spatial size 1x1; a 1x1 conv (Z18)                 */
+} ios_op_kind;
+
+enum {
+  IOS_F_RELU_POST = 1,          /* ReLU after the op (conv, sepconv, linear)        */
+  IOS_F_RELU_PRE = 2,           /* ReLU on the input (conv, global avgpool; implied for sepconv) */
+  IOS_F_CEIL_MODE = 4,          /* pooling output size rounds up (torch rule)         */
+  IOS_F_COUNT_INCLUDE_PAD = 8   /* avgpool divisor counts padding                     */
+};
+
+typedef struct {
+  int32_t kind;           /* ios_op_kind */
+  int32_t block;          /* block id: the DP runs per block; blocks must be contiguous
+                             in insertion order and edges may only go to the same or a later block */
+  int32_t out_channels;   /* conv/sepconv/linear: Cout; ignored (derived) for the other kinds      */
+  int32_t kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w;
+  int32_t flags;          /* IOS_F_* */
+  const float* weight;    /* host fp32, COPIED. conv: [Cout][Cin][kh][kw]; sepconv: depthwise [C][kh][kw]
+                             followed by pointwise [Cout][C]; linear: [Cout][Cin]; NULL otherwise   */
+  const float* bias;      /* host fp32 [Cout] or NULL (= 0), COPIED                                 */
+  const float* add_weights; /* host fp32 [n_inputs] or NULL (= 1.0) for ADD / SEPCONV, COPIED       */
+} ios_op_desc;
+
+typedef struct {
+  int32_t warmup;    /* untimed launches before the first trial (default 10)            */
+  int32_t trials;    /* timed trials; the median trial mean is returned (default 5)      */
+  int32_t reps;      /* back-to-back launches per trial between two CUDA events (default 20) */
+  int32_t l2_flush;  /* non-zero: write 2x the L2 size between trials                    */
+} ios_profile_opts;   /* DESIGN.md Z15 */
+
+/* ---- graph construction ------------------------------------------------------------------- */
+
+/* Creates G with op 0 = the graph input, an NCHW tensor [batch, c, h, w]. `device` is the CUDA
+ * ordinal later calls run on (not touched here). */
+IOS_API ios_status ios_graph_create(int32_t batch, int32_t c, int32_t h, int32_t w, ios_math math,
+                            int32_t device, ios_graph* out);
+
+/* Appends one op. `inputs` are existing op ids (0 = graph input), so insertion order is a
+ * topological order (the sequential schedule's order). Shapes are inferred; weights are
+ * copied. Writes the new op id (1, 2, ...) to *out_op_id. */
+IOS_API ios_status ios_add_op(ios_graph g, const ios_op_desc* d, const int32_t* inputs, int32_t n_inputs,
+                      int32_t* out_op_id);
+
+IOS_API ios_status ios_graph_num_ops(ios_graph g, int32_t* n_ops);   /* excludes the input op 0 */
+IOS_API ios_status ios_op_shape(ios_graph g, int32_t op, int32_t shape_nchw[4]);
+/* Block structure: the number of blocks, and for one block (by position) its ops in insertion order. */
+IOS_API ios_status ios_graph_num_blocks(ios_graph g, int32_t* n_blocks);
+IOS_API ios_status ios_graph_block_ops(ios_graph g, int32_t block_pos, int32_t* ops, int32_t cap, int32_t* n_ops,
+                               int32_t* block_id);
+/* 1 if the ops can be executed as one merged convolution (reading Z4), else 0. */
+IOS_API ios_status ios_stage_mergeable(ios_graph g, const int32_t* ops, int32_t n_ops, int32_t* mergeable);
+
+/* ---- measurement ---------------------------------------------------------------------------- */
+
+/* Latency in ms of running the stage {ops} (one block) with strategy t on the device: its groups
+ * (connected components) run concurrently inside ONE persistent launch, or the ops are
+ * merged into one convolution. Inputs of the stage are taken from the graph's
+ * activation buffers (synthetic contents). Synchronises. IOS_ERR_NOT_MERGEABLE for an illegal
+ * merge (GenerateStage turns that into L_merge = inf, Alg. 1 L28-29). opts may be NULL. */
+IOS_API ios_status ios_stage_latency(ios_graph g, const int32_t* ops, int32_t n_ops, ios_strategy t,
+                             const ios_profile_opts* opts, double* out_ms);
+
+/* ---- schedules ------------------------------------------------------------------------------ */
+
+/* Stage cost for the DP: milliseconds, INFINITY = illegal. `stage_mask` bit i = the i-th op of
+ * `block` in insertion order. Must be deterministic for bit-exact schedules. */
+typedef double (*ios_cost_fn)(void* ctx, int32_t block, uint64_t stage_mask, ios_strategy t);
+
+/* Algorithm 1 per block with pruning P(r, s) (r = max ops per group, s = max groups per stage;
+ * r or s <= 0 means unbounded), block schedules concatenated in block order. cost = NULL
+ * measures every distinct stage with ios_stage_latency (cached per (block, mask, T)).
+ * Ending order and ties: DESIGN.md Z1/Z2. *out_cost_ms = left fold of the stage costs. */
+IOS_API ios_status ios_schedule_dp(ios_graph g, int32_t r, int32_t s, ios_cost_fn cost, void* ctx,
+                           ios_schedule* out, double* out_cost_ms);
+/* Same with a strategy set (IOS-Both / IOS-Merge / IOS-Parallel) and optional search statistics
+ * (out_stats may be NULL): [0] states, [1] transitions, [2] distinct stages costed. */
+IOS_API ios_status ios_schedule_dp_ex(ios_graph g, int32_t r, int32_t s, ios_strategy_set set, ios_cost_fn cost,
+                              void* ctx, ios_schedule* out, double* out_cost_ms, int64_t out_stats[3]);
+IOS_API ios_status ios_schedule_sequential(ios_graph g, ios_schedule* out);  /* one op per stage   */
+IOS_API ios_status ios_schedule_greedy(ios_graph g, ios_schedule* out);      /* all ready ops       */
+/* Builds a schedule from explicit stages: stage i has stage_sizes[i] ops taken consecutively from
+ * `ops`, with strategy strategies[i]. Validated (IOS_ERR_BAD_SCHEDULE / IOS_ERR_NOT_MERGEABLE). */
+IOS_API ios_status ios_schedule_create(ios_graph g, int32_t n_stages, const int32_t* stage_sizes, const int32_t* ops,
+                               const int32_t* strategies, ios_schedule* out);
+IOS_API ios_status ios_schedule_num_stages(ios_schedule q, int32_t* n);
+IOS_API ios_status ios_schedule_stage(ios_schedule q, int32_t i, int32_t* ops, int32_t cap, int32_t* n_ops,
+                              ios_strategy* t, double* latency_ms);
+
+/* ---- execution ------------------------------------------------------------------------------ */
+
+/* Runs Q on `d_input` (device, caller-owned, NCHW fp32 [batch, c, h, w] contiguous) and writes the
+ * last op's output to `d_output` (device, caller-owned, NCHW fp32 contiguous). Stream-ordered and
+ * asynchronous on `cuda_stream` (a cudaStream_t; NULL = legacy default stream). The first call for
+ * a schedule builds its stage plans and captures them into a CUDA graph. */
+IOS_API ios_status ios_run(ios_graph g, ios_schedule q, const void* d_input, void* d_output, void* cuda_stream);
+/* Same with HOST buffers: copies the input in, runs, copies the output back, synchronises. */
+IOS_API ios_status ios_run_host(ios_graph g, ios_schedule q, const float* h_input, float* h_output, void* cuda_stream);
+/* Copies op `op`'s most recent output (NCHW fp32) to caller-owned device memory. */
+IOS_API ios_status ios_op_output(ios_graph g, int32_t op, void* d_out, void* cuda_stream);
+/* Number of kernel launches one ios_run of q performs (stage kernels + boundary layout kernels). */
+IOS_API ios_status ios_schedule_launches(ios_graph g, ios_schedule q, int32_t* n_launches);
+
+/* ---- stage-latency cache (checkpoint / resume of long searches) ------------------------------ */
+IOS_API ios_status ios_latency_cache_save(ios_graph g, const char* path);
+IOS_API ios_status ios_latency_cache_load(ios_graph g, const char* path);
+
+IOS_API const char* ios_last_error(void);
+IOS_API void ios_schedule_destroy(ios_schedule q);
+IOS_API void ios_graph_destroy(ios_graph g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IOS_H_ */

@@ -1,0 +1,710 @@
+// Device side of libios: activation memory plan (concat elision), weight packing, stage planning
+// (tile scheduler inputs), the CUDA-event stage profiler and the CUDA-graph runner.
+//
+//   stage plan: problems + tiles + dependency counters for one (block, mask, T)
+//   profiler    (A7, "directly measures the latencies"): W warm-up launches, then trials of R
+//               back-to-back launches between CUDA events; the median trial mean (Z15)
+//   runner      (A9): the stages of Q in order, captured once into a CUDA graph
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "ios_core.h"
+
+namespace ios {
+
+namespace {
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+struct OpDev {
+  View out{};                 // where the op's output lives (possibly a slice of a concat buffer)
+  bool elided = false;        // concat/identity realised by addressing alone
+  int alias_parent = -1;      // concat this op's output is a slice of
+  int alias_off = 0;          // channel offset inside the parent
+  void* wpack = nullptr;      // packed GEMM weights (conv / linear / sepconv pointwise)
+  int wpack_n8 = 0;           // packed rows (multiple of 8)
+  float* bias = nullptr;      // fp32, zero padded
+  float* dw = nullptr;        // sepconv depthwise weights fp32 [Cp_in][kh*kw]
+  float* add_w = nullptr;     // add / sepconv aggregation weights
+  View dw_out{};              // sepconv depthwise scratch (NHWC, Cp_in channels)
+};
+
+}  // namespace
+
+struct StagePlan {
+  StageDesc sd{};
+  int grid = 0;
+  bool empty = true;
+  void* dmem = nullptr;       // problems | views | segments
+  int* counters = nullptr;
+  void* workspace = nullptr;
+  void* merged_pack = nullptr;
+  float* merged_bias = nullptr;
+};
+
+struct DeviceState {
+  bool ready = false;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<OpDev> od;
+  std::vector<void*> allocs;
+  int* err = nullptr;
+  void* l2buf = nullptr;
+  int64_t l2bytes = 0;
+  std::map<std::tuple<int, uint64_t, int>, StagePlan*> plans;
+};
+
+namespace {
+
+void* dmalloc(DeviceState& d, size_t bytes) {
+  void* p = nullptr;
+  IOS_CHECK_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+  IOS_CHECK_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 256)));
+  d.allocs.push_back(p);
+  return p;
+}
+
+template <class T>
+T* upload(DeviceState& d, const std::vector<T>& v, size_t min_elems = 0) {
+  const size_t n = std::max(v.size(), min_elems);
+  T* p = static_cast<T*>(dmalloc(d, n * sizeof(T)));
+  if (!v.empty()) IOS_CHECK_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+uint32_t tf32_rne_bits(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return u;   // inf / nan
+  u += 0xFFFu + ((u >> 13) & 1u);
+  return u & ~0x1FFFu;
+}
+uint16_t bf16_rne_bits(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)(u >> 16);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+// Packs a GEMM weight matrix w(n, k), n < N, k < K, into the UMMA K-major SWIZZLE_NONE smem image
+// order: [k chunk][n / 8][8 pieces of 16 B][n % 8][16 B]. Any BN rows starting at a multiple of 8
+// of one chunk are then one contiguous run of BN * 128 bytes (one cp.async.bulk).
+template <class F>
+void* pack_gemm(DeviceState& d, int N, int K, bool bf16, F w, int* n8_out) {
+  const int esz = bf16 ? 2 : 4, elems = kChunkBytes / esz, vec = 16 / esz;
+  const int kch = (K + elems - 1) / elems;
+  const int n8 = round_up(N, 8);
+  std::vector<uint8_t> buf((size_t)kch * n8 * kChunkBytes, 0);
+  for (int n = 0; n < N; ++n) {
+    for (int k = 0; k < K; ++k) {
+      const float v = w(n, k);
+      if (v == 0.0f) continue;
+      const int c = k / elems, kk = k % elems, pc = kk / vec, e = kk % vec;
+      const size_t off = (((size_t)c * (n8 / 8) + n / 8) * 8 + pc) * 128 + (n % 8) * 16 + e * esz;
+      if (bf16) {
+        const uint16_t b = bf16_rne_bits(v);
+        std::memcpy(&buf[off], &b, 2);
+      } else {
+        const uint32_t b = tf32_rne_bits(v);
+        std::memcpy(&buf[off], &b, 4);
+      }
+    }
+  }
+  *n8_out = n8;
+  return upload(d, buf);
+}
+
+int64_t view_elems(const Op& o, int C) { return (int64_t)o.N * o.H * o.W * C; }
+
+void ensure_device(Graph& g) {
+  if (g.dev && g.dev->ready) return;
+  if (!g.dev) g.dev = new DeviceState();
+  DeviceState& d = *g.dev;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= g.device)
+    IOS_FAIL(IOS_ERR_CUDA, "no CUDA device " + std::to_string(g.device) + " (the engine has no CPU fallback)");
+  IOS_CHECK_CUDA(cudaSetDevice(g.device));
+  cudaDeviceProp prop;
+  IOS_CHECK_CUDA(cudaGetDeviceProperties(&prop, g.device));
+  if (prop.major != 10 || prop.minor != 0)
+    IOS_FAIL(IOS_ERR_CUDA, std::string("libios is built for sm_100a; device is ") + prop.name);
+  d.num_sms = prop.multiProcessorCount;
+  IOS_CHECK_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  IOS_CHECK_CUDA(cudaEventCreate(&d.ev0));
+  IOS_CHECK_CUDA(cudaEventCreate(&d.ev1));
+  d.err = static_cast<int*>(dmalloc(d, 16));
+  d.l2bytes = 2 * (int64_t)prop.l2CacheSize;
+
+  const int n = (int)g.ops.size();
+  d.od.assign(n, OpDev{});
+  // ---- concat elision: producers write straight into channel slices of the concat's buffer.
+  // Outer (later) concats first, so nested concats resolve top-down.
+  for (int v = n - 1; v >= 1; --v) {
+    const Op& o = g.ops[v];
+    if (o.kind != IOS_OP_CONCAT) continue;
+    bool ok = true;
+    for (size_t i = 0; i < o.inputs.size() && ok; ++i) {
+      const int u = o.inputs[i];
+      if (u == 0 || d.od[u].alias_parent >= 0 || g.ops[u].C % 8 != 0) ok = false;
+      for (size_t j = 0; j < i; ++j)
+        if (o.inputs[j] == u) ok = false;
+    }
+    if (!ok) continue;
+    int off = 0;
+    for (int u : o.inputs) {
+      d.od[u].alias_parent = v;
+      d.od[u].alias_off = off;
+      off += g.ops[u].C;
+    }
+    d.od[v].elided = true;
+  }
+  // ---- allocate root buffers, then resolve views top-down (parents have larger ids)
+  for (int v = 0; v < n; ++v) {
+    if (d.od[v].alias_parent >= 0) continue;
+    const Op& o = g.ops[v];
+    void* p = dmalloc(d, view_elems(o, o.Cp) * g.esize());
+    d.od[v].out = View{(uint64_t)p, o.Cp, 0, o.Cp, o.C, o.H, o.W};
+  }
+  for (int v = n - 1; v >= 0; --v) {
+    if (d.od[v].alias_parent < 0) continue;
+    // parents are resolved first because they have larger ids and we walk downwards
+    const View& pv = d.od[d.od[v].alias_parent].out;
+    const Op& o = g.ops[v];
+    d.od[v].out = View{pv.ptr, pv.cstride, pv.coff + d.od[v].alias_off, o.Cp, o.C, o.H, o.W};
+  }
+  // identities not written into a concat are pure aliases of their input
+  for (int v = 1; v < n; ++v) {
+    const Op& o = g.ops[v];
+    if (o.kind == IOS_OP_IDENTITY && d.od[v].alias_parent < 0) {
+      d.od[v].out = d.od[o.inputs[0]].out;
+      d.od[v].elided = true;
+    }
+  }
+  // ---- weights
+  const bool bf16 = g.math == IOS_MATH_BF16;
+  for (int v = 1; v < n; ++v) {
+    const Op& o = g.ops[v];
+    OpDev& e = d.od[v];
+    const Op& x = g.ops[o.inputs[0]];
+    if (!o.add_w.empty()) e.add_w = upload(d, o.add_w);
+    if (o.kind == IOS_OP_CONV || o.kind == IOS_OP_LINEAR) {
+      const int cin = x.C, cin_p = x.Cp, kh = o.kh, kw = o.kw;
+      const float* W = o.weight.data();
+      e.wpack = pack_gemm(d, o.Cp, kh * kw * cin_p, bf16, [&](int nn, int k) -> float {
+        if (nn >= o.cout) return 0.0f;
+        const int tap = k / cin_p, ci = k % cin_p;
+        if (ci >= cin) return 0.0f;
+        const int i = tap / kw, j = tap % kw;
+        return W[(((size_t)nn * cin + ci) * kh + i) * kw + j];
+      }, &e.wpack_n8);
+      std::vector<float> b(o.bias);
+      e.bias = upload(d, b, (size_t)round_up(o.Cp, 256) + 16);
+    } else if (o.kind == IOS_OP_SEPCONV) {
+      const int c = x.C, cp = x.Cp, kk = o.kh * o.kw;
+      std::vector<float> dw((size_t)cp * kk, 0.0f);
+      for (int ch = 0; ch < c; ++ch)
+        for (int t = 0; t < kk; ++t) dw[(size_t)ch * kk + t] = o.weight[(size_t)ch * kk + t];
+      e.dw = upload(d, dw);
+      const float* PW = o.weight.data() + (size_t)c * kk;
+      e.wpack = pack_gemm(d, o.Cp, cp, bf16, [&](int nn, int k) -> float {
+        return (nn < o.cout && k < c) ? PW[(size_t)nn * c + k] : 0.0f;
+      }, &e.wpack_n8);
+      std::vector<float> b(o.bias);
+      e.bias = upload(d, b, (size_t)round_up(o.Cp, 256) + 16);
+      void* p = dmalloc(d, (size_t)o.N * o.H * o.W * cp * g.esize());
+      e.dw_out = View{(uint64_t)p, cp, 0, cp, c, o.H, o.W};
+    }
+  }
+  d.ready = true;
+}
+
+// ------------------------------------------------------------------------------ stage planning
+struct GemmSpec {
+  int M, N16, K, kch;
+  int BN, ntn, mt, split, cps;
+};
+
+void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
+  for (GemmSpec* p : gs) {
+    p->mt = (p->M + kBM - 1) / kBM;
+    if (p->N16 <= kMaxBN) {
+      p->BN = p->N16;
+    } else {
+      const int nt = (p->N16 + kMaxBN - 1) / kMaxBN;
+      p->BN = round_up((p->N16 + nt - 1) / nt, 16);
+    }
+    p->ntn = (p->N16 + p->BN - 1) / p->BN;
+    p->split = 1;
+    p->cps = p->kch;
+  }
+  // Fill the SMs: refine the problem with the most expensive tile (N halving first, then split-K)
+  // until there are about as many units as SMs.
+  for (int it = 0; it < 256; ++it) {
+    int units = simt_tiles;
+    for (GemmSpec* p : gs) units += p->mt * p->ntn * p->split;
+    if (units >= num_sms) break;
+    GemmSpec* best = nullptr;
+    double best_cost = 0;
+    for (GemmSpec* p : gs) {
+      const bool can_n = p->BN >= 128;
+      const bool can_k = p->cps >= 4 && p->split < 32;
+      if (!can_n && !can_k) continue;
+      const double c = p->cps * (1.0 + p->BN / 256.0);
+      if (c > best_cost) {
+        best_cost = c;
+        best = p;
+      }
+    }
+    if (!best) break;
+    if (best->BN >= 128) {
+      best->BN = round_up(best->BN / 2, 16);
+      best->ntn = (best->N16 + best->BN - 1) / best->BN;
+    } else {
+      const int want = best->split * 2;
+      best->cps = (best->kch + want - 1) / want;
+      best->split = (best->kch + best->cps - 1) / best->cps;
+    }
+  }
+}
+
+struct PlanBuilder {
+  Graph& g;
+  DeviceState& d;
+  std::vector<Problem> probs;
+  std::vector<View> views;
+  std::vector<Segment> segs;
+  std::vector<GemmSpec> specs;       // parallel to probs (GEMM problems only meaningful)
+  std::map<int, std::vector<int>> op_probs;  // op -> its problems (last one produces the output)
+
+  explicit PlanBuilder(Graph& gg) : g(gg), d(*gg.dev) {}
+
+  int add_problem(int kind) {
+    Problem p{};
+    p.kind = kind;
+    p.dtype = g.dtype();
+    p.split = 1;
+    probs.push_back(p);
+    specs.push_back(GemmSpec{});
+    return (int)probs.size() - 1;
+  }
+  // completion counters of the in-stage producers of op u's output (through elided ops)
+  void producers(int u, const std::vector<int>& stage_ops, std::vector<int>& out) {
+    if (u == 0 || !std::binary_search(stage_ops.begin(), stage_ops.end(), u)) return;
+    auto it = op_probs.find(u);
+    if (it != op_probs.end() && !it->second.empty()) {
+      out.push_back(it->second.back());
+      return;
+    }
+    for (int w : g.ops[u].inputs) producers(w, stage_ops, out);   // elided concat / identity
+  }
+  void add_deps(int pi, const std::vector<int>& deps) {
+    Problem& p = probs[pi];
+    for (int q : deps) {
+      bool dup = false;
+      for (int k = 0; k < p.n_deps; ++k) dup |= p.dep_idx[k] == q;
+      if (dup) continue;
+      if (p.n_deps >= 6) IOS_FAIL(IOS_ERR_UNSUPPORTED, "stage member with more than 6 in-stage producers");
+      p.dep_idx[p.n_deps++] = q;   // problem index for now; turned into counter index later
+    }
+  }
+  int gemm(int in_op_view_src, const View& in, void* wpack, int n8, float* bias, int Ntot, int kh, int kw, int sh,
+           int sw, int ph, int pw, int Ho, int Wo, int flags) {
+    (void)in_op_view_src;
+    const int pi = add_problem(PK_GEMM);
+    Problem& p = probs[pi];
+    p.batch = g.batch;
+    p.flags = flags;
+    p.kh = kh; p.kw = kw; p.sh = sh; p.sw = sw; p.ph = ph; p.pw = pw;
+    p.Ho = Ho; p.Wo = Wo;
+    p.in_begin = (int)views.size();
+    p.n_in = 1;
+    views.push_back(in);
+    p.wts = (uint64_t)wpack;
+    p.Npad8 = n8;
+    p.bias = (uint64_t)bias;
+    p.M = g.batch * Ho * Wo;
+    p.K = kh * kw * in.C;
+    const int elems = kChunkBytes / g.esize();
+    p.k_chunks = (p.K + elems - 1) / elems;
+    p.seg_begin = (int)segs.size();
+    GemmSpec& s = specs[pi];
+    s.M = p.M;
+    s.N16 = round_up(Ntot, 16);
+    s.K = p.K;
+    s.kch = p.k_chunks;
+    return pi;
+  }
+  void seg(int pi, int n0, int n1, const View& out, int relu) {
+    Segment s{};
+    s.n0 = n0;
+    s.n1 = n1;
+    s.out = out;
+    s.relu = relu;
+    segs.push_back(s);
+    probs[pi].n_seg++;
+  }
+  int simt(int kind, const Op& o, const std::vector<int>& inputs, const View& out, int flags) {
+    const int pi = add_problem(kind);
+    Problem& p = probs[pi];
+    p.batch = g.batch;
+    p.flags = flags;
+    p.kh = o.kh; p.kw = o.kw; p.sh = o.sh; p.sw = o.sw; p.ph = o.ph; p.pw = o.pw;
+    p.Ho = o.H; p.Wo = o.W;
+    p.in_begin = (int)views.size();
+    p.n_in = (int)inputs.size();
+    for (int u : inputs) views.push_back(d.od[u].out);
+    p.out = out;
+    return pi;
+  }
+};
+
+StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
+  DeviceState& d = *g.dev;
+  const std::vector<int> ops = g.ops_of(bpos, mask);
+  PlanBuilder b(g);
+  auto* plan = new StagePlan();
+  try {
+    if (strategy == IOS_MERGE) {
+      // ---- operator merge (Z4): bounding-box kernel, stacked zero-padded filters,
+      // one GEMM; the split is the epilogue writing each branch's channel slice.
+      if (!g.mergeable(ops)) IOS_FAIL(IOS_ERR_NOT_MERGEABLE, "stage is not mergeable");
+      int st_h = 1 << 30, en_h = -(1 << 30), st_w = 1 << 30, en_w = -(1 << 30);
+      for (int v : ops) {
+        const Op& o = g.ops[v];
+        st_h = std::min(st_h, -o.ph); en_h = std::max(en_h, -o.ph + o.kh);
+        st_w = std::min(st_w, -o.pw); en_w = std::max(en_w, -o.pw + o.kw);
+      }
+      const int KH = en_h - st_h, KW = en_w - st_w, PH = -st_h, PW = -st_w;
+      const Op& f = g.ops[ops[0]];
+      const Op& x = g.ops[f.inputs[0]];
+      std::vector<int> row0;
+      int ntot = 0;
+      for (int v : ops) {
+        row0.push_back(ntot);
+        ntot += g.ops[v].Cp;
+      }
+      const int cin = x.C, cin_p = x.Cp;
+      int merged_n8 = 0;
+      plan->merged_pack = pack_gemm(d, ntot, KH * KW * cin_p, g.math == IOS_MATH_BF16, [&](int nn, int k) -> float {
+        int bi = (int)ops.size() - 1;
+        while (row0[bi] > nn) --bi;
+        const Op& o = g.ops[ops[bi]];
+        const int r = nn - row0[bi];
+        if (r >= o.cout) return 0.0f;
+        const int tap = k / cin_p, ci = k % cin_p;
+        if (ci >= cin) return 0.0f;
+        const int i = tap / KW - (-o.ph - st_h), j = tap % KW - (-o.pw - st_w);
+        if (i < 0 || i >= o.kh || j < 0 || j >= o.kw) return 0.0f;
+        return o.weight[(((size_t)r * cin + ci) * o.kh + i) * o.kw + j];
+      }, &merged_n8);
+      std::vector<float> bias((size_t)round_up(ntot, 256) + 16, 0.0f);
+      for (size_t bi = 0; bi < ops.size(); ++bi) {
+        const Op& o = g.ops[ops[bi]];
+        for (int c = 0; c < o.cout; ++c) bias[row0[bi] + c] = o.bias[c];
+      }
+      plan->merged_bias = upload(d, bias);
+      const int pi = b.gemm(f.inputs[0], d.od[f.inputs[0]].out, plan->merged_pack, merged_n8, plan->merged_bias,
+                            ntot, KH, KW, f.sh, f.sw, PH, PW, f.H, f.W, f.flags & IOS_F_RELU_PRE);
+      for (size_t bi = 0; bi < ops.size(); ++bi) {
+        const Op& o = g.ops[ops[bi]];
+        b.seg(pi, row0[bi], row0[bi] + o.Cp, d.od[ops[bi]].out, (o.flags & IOS_F_RELU_POST) ? 1 : 0);
+      }
+      for (int v : ops) b.op_probs[v] = {pi};
+    } else {
+      // ---- concurrent execution: every member op in one launch; groups emerge from dependencies
+      for (int v : ops) {
+        const Op& o = g.ops[v];
+        OpDev& e = d.od[v];
+        std::vector<int> deps;
+        for (int u : o.inputs) b.producers(u, ops, deps);
+        switch (o.kind) {
+          case IOS_OP_CONV:
+          case IOS_OP_LINEAR: {
+            const int u = o.inputs[0];
+            const int pi = b.gemm(u, d.od[u].out, e.wpack, e.wpack_n8, e.bias, o.Cp, o.kh, o.kw, o.sh, o.sw, o.ph, o.pw,
+                                  o.H, o.W, o.flags & IOS_F_RELU_PRE);
+            b.seg(pi, 0, o.Cp, e.out, (o.flags & IOS_F_RELU_POST) ? 1 : 0);
+            b.add_deps(pi, deps);
+            b.op_probs[v] = {pi};
+            break;
+          }
+          case IOS_OP_SEPCONV: {
+            Op dwop = o;
+            const int pd = b.simt(PK_DWCONV, dwop, o.inputs, e.dw_out, o.flags);
+            b.probs[pd].wts = (uint64_t)e.dw;
+            b.probs[pd].add_w = (uint64_t)e.add_w;
+            b.add_deps(pd, deps);
+            const int pi = b.gemm(-1, e.dw_out, e.wpack, e.wpack_n8, e.bias, o.Cp, 1, 1, 1, 1, 0, 0, o.H, o.W, 0);
+            b.seg(pi, 0, o.Cp, e.out, (o.flags & IOS_F_RELU_POST) ? 1 : 0);
+            b.add_deps(pi, {pd});
+            b.op_probs[v] = {pd, pi};
+            break;
+          }
+          case IOS_OP_MAXPOOL:
+          case IOS_OP_AVGPOOL:
+          case IOS_OP_GLOBAL_AVGPOOL:
+          case IOS_OP_ADD: {
+            const int kind = o.kind == IOS_OP_MAXPOOL ? PK_MAXPOOL
+                             : o.kind == IOS_OP_AVGPOOL ? PK_AVGPOOL
+                             : o.kind == IOS_OP_ADD ? PK_ADD : PK_GAVGPOOL;
+            const int pi = b.simt(kind, o, o.inputs, e.out, o.flags);
+            b.probs[pi].add_w = (uint64_t)e.add_w;
+            b.add_deps(pi, deps);
+            b.op_probs[v] = {pi};
+            break;
+          }
+          case IOS_OP_CONCAT:
+          case IOS_OP_IDENTITY: {
+            if (e.elided) break;   // realised by addressing: no work, completion = its producers'
+            const int pi = b.simt(PK_COPY, o, o.inputs, e.out, o.flags);
+            b.add_deps(pi, deps);
+            b.op_probs[v] = {pi};
+            break;
+          }
+          default:
+            IOS_FAIL(IOS_ERR_UNSUPPORTED, "op kind");
+        }
+      }
+    }
+    // ---- tiling
+    const int nv = 16 / g.esize();
+    int simt_tiles = 0;
+    for (size_t i = 0; i < b.probs.size(); ++i) {
+      Problem& p = b.probs[i];
+      if (p.kind == PK_GEMM) continue;
+      const int nvec = p.out.C / nv;
+      if (p.kind == PK_GAVGPOOL) {
+        p.n_items = p.batch * nvec;
+        p.items_per_tile = 128;
+      } else {
+        p.n_items = p.batch * p.Ho * p.Wo;
+        p.items_per_tile = std::max(1, 2048 / std::max(1, nvec));
+      }
+      p.n_tiles = (p.n_items + p.items_per_tile - 1) / p.items_per_tile;
+      simt_tiles += p.n_tiles;
+    }
+    std::vector<GemmSpec*> gs;
+    for (size_t i = 0; i < b.probs.size(); ++i)
+      if (b.probs[i].kind == PK_GEMM) gs.push_back(&b.specs[i]);
+    choose_tiling(gs, simt_tiles, d.num_sms);
+    size_t ws_bytes = 0;
+    int n_tilectr = 0;
+    for (size_t i = 0; i < b.probs.size(); ++i) {
+      Problem& p = b.probs[i];
+      if (p.kind != PK_GEMM) continue;
+      const GemmSpec& s = b.specs[i];
+      p.BN = s.BN;
+      p.n_tiles_n = s.ntn;
+      p.m_tiles = s.mt;
+      p.split = s.split;
+      p.chunks_per_split = s.cps;
+      p.n_tiles = s.mt * s.ntn * s.split;
+      if (p.split > 1) {
+        p.workspace = ws_bytes;   // offset for now
+        ws_bytes += (size_t)s.mt * s.ntn * s.split * kBM * s.BN * sizeof(float);
+        p.tilectr_idx = n_tilectr;
+        n_tilectr += s.mt * s.ntn;
+      }
+    }
+    // ---- tiles and counters: problems keep insertion (topological) order, so deps point back
+    const int np = (int)b.probs.size();
+    if (np > kMaxProblems) IOS_FAIL(IOS_ERR_UNSUPPORTED, "too many problems in one stage");
+    int tiles = 0;
+    for (Problem& p : b.probs) {
+      p.tile_begin = tiles;
+      tiles += p.n_tiles;
+    }
+    const int n_counters = 1 + np + n_tilectr;
+    for (int i = 0; i < np; ++i) {
+      Problem& p = b.probs[i];
+      p.done_idx = 1 + i;
+      for (int k = 0; k < p.n_deps; ++k) {
+        const Problem& q = b.probs[p.dep_idx[k]];
+        p.dep_target[k] = q.kind == PK_GEMM ? q.m_tiles * q.n_tiles_n : q.n_tiles;
+        p.dep_idx[k] = 1 + p.dep_idx[k];
+      }
+      if (p.kind == PK_GEMM && p.split > 1) p.tilectr_idx += 1 + np;
+    }
+    plan->empty = tiles == 0;
+    if (!plan->empty) {
+      if (ws_bytes) plan->workspace = dmalloc(d, ws_bytes);
+      for (Problem& p : b.probs)
+        if (p.kind == PK_GEMM && p.split > 1) p.workspace += (uint64_t)plan->workspace;
+      const size_t pb = b.probs.size() * sizeof(Problem), vb = b.views.size() * sizeof(View),
+                   sb = b.segs.size() * sizeof(Segment);
+      std::vector<uint8_t> blob(pb + vb + sb + 64, 0);
+      std::memcpy(blob.data(), b.probs.data(), pb);
+      if (vb) std::memcpy(blob.data() + pb, b.views.data(), vb);
+      if (sb) std::memcpy(blob.data() + pb + vb, b.segs.data(), sb);
+      plan->dmem = upload(d, blob);
+      plan->counters = static_cast<int*>(dmalloc(d, (size_t)n_counters * sizeof(int)));
+      StageDesc& sd = plan->sd;
+      sd.problems = (uint64_t)plan->dmem;
+      sd.views = (uint64_t)plan->dmem + pb;
+      sd.segs = (uint64_t)plan->dmem + pb + vb;
+      sd.counters = (uint64_t)plan->counters;
+      sd.err = (uint64_t)d.err;
+      sd.n_problems = np;
+      sd.n_tiles = tiles;
+      sd.n_counters = n_counters;
+      sd.has_gemm = 0;
+      for (Problem& p : b.probs) sd.has_gemm |= p.kind == PK_GEMM;
+      plan->grid = std::min(tiles, d.num_sms);
+    }
+  } catch (...) {
+    delete plan;
+    throw;
+  }
+  return plan;
+}
+
+StagePlan* get_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
+  DeviceState& d = *g.dev;
+  auto key = std::make_tuple(bpos, mask, strategy);
+  auto it = d.plans.find(key);
+  if (it != d.plans.end()) return it->second;
+  StagePlan* p = build_plan(g, bpos, mask, strategy);
+  d.plans[key] = p;
+  return p;
+}
+
+void launch_plan(const StagePlan* p, cudaStream_t st) {
+  if (p->empty) return;
+  IOS_CHECK_CUDA(launch_stage(p->sd, p->grid, st));
+}
+
+void check_err(DeviceState& d) {
+  int h = 0;
+  IOS_CHECK_CUDA(cudaMemcpy(&h, d.err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) {
+    IOS_CHECK_CUDA(cudaMemset(d.err, 0, sizeof(int)));
+    IOS_FAIL(IOS_ERR_KERNEL, "in-kernel dependency wait timed out");
+  }
+}
+
+}  // namespace
+
+double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const ios_profile_opts* opts) {
+  ensure_device(g);
+  DeviceState& d = *g.dev;
+  int bpos = -1;
+  const uint64_t mask = g.mask_of(ops, &bpos);
+  const int warmup = opts && opts->warmup > 0 ? opts->warmup : 10;
+  const int trials = opts && opts->trials > 0 ? opts->trials : 5;
+  const int reps = opts && opts->reps > 0 ? opts->reps : 20;
+  const bool flush = opts && opts->l2_flush;
+  StagePlan* p;
+  try {
+    p = get_plan(g, bpos, mask, strategy);
+  } catch (const Error& e) {
+    if (e.code != IOS_ERR_UNSUPPORTED) throw;
+    g.latency_cache[std::make_tuple(bpos, mask, strategy)] = kInf;   // not executable -> never chosen
+    return kInf;
+  }
+  double ms = 0.0;
+  if (!p->empty) {
+    if (flush && !d.l2buf) d.l2buf = dmalloc(d, (size_t)d.l2bytes);
+    for (int i = 0; i < warmup; ++i) launch_plan(p, d.stream);
+    std::vector<double> t;
+    for (int tr = 0; tr < trials; ++tr) {
+      if (flush) IOS_CHECK_CUDA(launch_l2_flush(d.l2buf, d.l2bytes, d.stream));
+      IOS_CHECK_CUDA(cudaEventRecord(d.ev0, d.stream));
+      for (int i = 0; i < reps; ++i) launch_plan(p, d.stream);
+      IOS_CHECK_CUDA(cudaEventRecord(d.ev1, d.stream));
+      IOS_CHECK_CUDA(cudaEventSynchronize(d.ev1));
+      float e = 0;
+      IOS_CHECK_CUDA(cudaEventElapsedTime(&e, d.ev0, d.ev1));
+      t.push_back((double)e / reps);
+    }
+    check_err(d);
+    std::sort(t.begin(), t.end());
+    ms = t[t.size() / 2];
+  }
+  g.latency_cache[std::make_tuple(bpos, mask, strategy)] = ms;
+  return ms;
+}
+
+void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStream_t st) {
+  ensure_device(g);
+  DeviceState& d = *g.dev;
+  if (!q.exec || q.exec_in != d_in || q.exec_out != d_out) {
+    destroy_schedule_exec(q);
+    std::vector<StagePlan*> plans;
+    for (const Stage& s : q.stages) {
+      int bpos = -1;
+      const uint64_t mask = g.mask_of(s.ops, &bpos);
+      plans.push_back(get_plan(g, bpos, mask, s.strategy));
+    }
+    const Op& in = g.ops[0];
+    const Op& last = g.ops.back();
+    IOS_CHECK_CUDA(cudaStreamBeginCapture(d.stream, cudaStreamCaptureModeThreadLocal));
+    int launches = 0;
+    cudaError_t e = launch_nchw_to_nhwc(static_cast<const float*>(d_in), d.od[0].out, g.dtype(), in.N, in.C, d.stream);
+    ++launches;
+    for (StagePlan* p : plans) {
+      if (e != cudaSuccess) break;
+      if (p->empty) continue;
+      e = launch_stage(p->sd, p->grid, d.stream);
+      ++launches;
+    }
+    if (e == cudaSuccess) {
+      e = launch_nhwc_to_nchw(d.od[last.id].out, g.dtype(), static_cast<float*>(d_out), last.N, last.C, d.stream);
+      ++launches;
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(d.stream, &graph);
+    if (e != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      IOS_CHECK_CUDA(e);
+    }
+    IOS_CHECK_CUDA(e2);
+    q.graph = graph;
+    IOS_CHECK_CUDA(cudaGraphInstantiate(&q.exec, graph, 0));
+    q.exec_in = d_in;
+    q.exec_out = d_out;
+    q.n_launches = launches;
+  }
+  IOS_CHECK_CUDA(cudaGraphLaunch(q.exec, st));
+}
+
+int schedule_launches(Graph& g, Schedule& q) {
+  ensure_device(g);
+  int n = 2;
+  for (const Stage& s : q.stages) {
+    int bpos = -1;
+    const uint64_t mask = g.mask_of(s.ops, &bpos);
+    if (!get_plan(g, bpos, mask, s.strategy)->empty) ++n;
+  }
+  return n;
+}
+
+void op_output(Graph& g, int op, void* d_out, cudaStream_t st) {
+  ensure_device(g);
+  const Op& o = g.ops[op];
+  IOS_CHECK_CUDA(launch_nhwc_to_nchw(g.dev->od[op].out, g.dtype(), static_cast<float*>(d_out), o.N, o.C, st));
+}
+
+void destroy_schedule_exec(Schedule& q) {
+  if (q.exec) cudaGraphExecDestroy(q.exec);
+  if (q.graph) cudaGraphDestroy(q.graph);
+  q.exec = nullptr;
+  q.graph = nullptr;
+}
+
+void destroy_device(Graph& g) {
+  if (!g.dev) return;
+  DeviceState& d = *g.dev;
+  for (auto& [k, p] : d.plans) delete p;
+  for (void* p : d.allocs) cudaFree(p);
+  if (d.ev0) cudaEventDestroy(d.ev0);
+  if (d.ev1) cudaEventDestroy(d.ev1);
+  if (d.stream) cudaStreamDestroy(d.stream);
+  delete g.dev;
+  g.dev = nullptr;
+}
+
+}  // namespace ios

@@ -1,0 +1,186 @@
+// Inter-Operator Scheduler: Algorithm 1 per block with pruning P(r, s).
+//
+// States S and endings S' are 64-bit masks over one block (bit i = i-th op of the block in
+// insertion order). Endings are enumerated directly (never by scanning all subsets): ops of S are
+// visited in descending index order — a reverse topological order — and op u may join S' only
+// if all its successors inside S are already in S' (the ending condition P:237-239). The r bound
+// prunes during enumeration (a group only grows as ops are added); the s bound is checked on
+// complete endings. Endings are then sorted canonically (|S'| ascending, mask descending; DESIGN.md
+// Z1) and the first minimiser wins (strict < at L19). GenerateStage: ties go to merge (L30, Z2).
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <limits>
+
+#include "ios_core.h"
+
+namespace ios {
+
+namespace {
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+struct Memo {
+  double cost;
+  uint64_t choice;
+  int strategy;
+};
+
+class BlockDP {
+ public:
+  BlockDP(const Graph& g, int bpos, int r, int s, int set, std::function<double(uint64_t, int)> cost)
+      : g_(g), b_(g.blocks[bpos]), bpos_(bpos), r_(r), s_(s), set_(set), cost_(std::move(cost)) {}
+
+  double run(std::vector<std::pair<uint64_t, int>>* q) {
+    const int n = (int)b_.ops.size();
+    const uint64_t v = n == 64 ? ~0ull : ((1ull << n) - 1);
+    const double total = scheduler(v);                       // L5
+    q->clear();                                              // L6
+    uint64_t s = v;                                          // L7
+    while (s) {                                              // L8
+      const Memo& m = memo_.at(s);                           // L9
+      q->insert(q->begin(), {m.choice, m.strategy});         // L10
+      s &= ~m.choice;                                        // L11
+    }
+    return total;                                            // L12
+  }
+  int64_t states() const { return (int64_t)memo_.size() + 1; }
+  int64_t transitions() const { return transitions_; }
+
+ private:
+  // component (group) of op u inside set `m`
+  uint64_t component_of(int u, uint64_t m) const {
+    uint64_t comp = 1ull << u, frontier = comp;
+    while (frontier) {
+      const int x = __builtin_ctzll(frontier);
+      frontier &= frontier - 1;
+      const uint64_t nb = (b_.succ[x] | b_.pred[x]) & m & ~comp;
+      comp |= nb;
+      frontier |= nb;
+    }
+    return comp;
+  }
+
+  void enumerate(const std::vector<int>& bits, size_t pos, uint64_t S, uint64_t chosen, std::vector<uint64_t>& out) const {
+    if (pos == bits.size()) {
+      if (!chosen) return;
+      if (s_ > 0 && (int)g_.components(bpos_, chosen).size() > s_) return;   // at most s groups
+      out.push_back(chosen);
+      return;
+    }
+    const int u = bits[pos];
+    enumerate(bits, pos + 1, S, chosen, out);                                 // u stays in S - S'
+    if ((b_.succ[u] & S & ~chosen) == 0) {                                    // all successors already in S'
+      const uint64_t nc = chosen | (1ull << u);
+      if (r_ > 0 && popcount64(component_of(u, nc)) > r_) return;             // a group of > r ops
+      enumerate(bits, pos + 1, S, nc, out);
+    }
+  }
+
+  std::vector<uint64_t> endings(uint64_t S) const {
+    std::vector<int> bits;
+    for (uint64_t m = S; m; m &= m - 1) bits.push_back(__builtin_ctzll(m));
+    std::reverse(bits.begin(), bits.end());                                   // descending index
+    std::vector<uint64_t> out;
+    enumerate(bits, 0, S, 0, out);
+    std::sort(out.begin(), out.end(), [](uint64_t a, uint64_t b) {
+      const int pa = popcount64(a), pb = popcount64(b);
+      return pa != pb ? pa < pb : a > b;
+    });
+    return out;
+  }
+
+  std::pair<double, int> generate_stage(uint64_t sp) {                        // L23-33
+    double l_conc, l_merge;
+    if (set_ == IOS_MERGE_ONLY && popcount64(sp) > 1) l_conc = kInf;
+    else l_conc = cost_(sp, IOS_CONCURRENT);                                  // L24-25
+    if (set_ != IOS_PARALLEL_ONLY && g_.mergeable(g_.ops_of(bpos_, sp)))      // L26
+      l_merge = cost_(sp, IOS_MERGE);                                         // L27
+    else
+      l_merge = kInf;                                                         // L28-29
+    if (std::isnan(l_conc)) l_conc = kInf;
+    if (std::isnan(l_merge)) l_merge = kInf;
+    if (l_conc < l_merge) return {l_conc, IOS_CONCURRENT};                    // L30-31
+    return {l_merge, IOS_MERGE};                                              // L32-33
+  }
+
+  double scheduler(uint64_t S) {                                              // L13
+    if (S == 0) return 0.0;                                                   // cost[empty] = 0 (L1)
+    auto it = memo_.find(S);
+    if (it != memo_.end()) return it->second.cost;                            // L14-15
+    double best = kInf;
+    uint64_t best_sp = 0;
+    int best_t = IOS_CONCURRENT;
+    const std::vector<uint64_t> ends = endings(S);
+    for (uint64_t sp : ends) {                                                // L16
+      ++transitions_;
+      const auto [l_sp, t_sp] = generate_stage(sp);                           // L17
+      const double l_s = scheduler(S & ~sp) + l_sp;                           // L18
+      if (l_s < best) {                                                       // L19
+        best = l_s;                                                           // L20
+        best_sp = sp;                                                         // L21
+        best_t = t_sp;
+      }
+    }
+    memo_[S] = Memo{best, best_sp, best_t};
+    return best;                                                              // L22
+  }
+
+  const Graph& g_;
+  const BlockInfo& b_;
+  int bpos_, r_, s_, set_;
+  std::function<double(uint64_t, int)> cost_;
+  std::unordered_map<uint64_t, Memo> memo_;
+  int64_t transitions_ = 0;
+};
+
+}  // namespace
+
+// InterOperatorScheduler over every block, schedules concatenated in block order.
+double schedule_dp(Graph& g, int r, int s, int set, ios_cost_fn cost, void* ctx, Schedule* out, int64_t stats[3]) {
+  double total = 0.0;
+  out->stages.clear();
+  int64_t n_states = 0, n_trans = 0, n_costed = 0;
+  for (int bp = 0; bp < (int)g.blocks.size(); ++bp) {
+    const int block_id = g.blocks[bp].id;
+    std::map<std::pair<uint64_t, int>, double> local;   // per-call cache of callback costs
+    auto fn = [&](uint64_t mask, int t) -> double {
+      if (cost) {
+        auto key = std::make_pair(mask, t);
+        auto it = local.find(key);
+        if (it != local.end()) return it->second;
+        const double v = cost(ctx, block_id, mask, (ios_strategy)t);
+        local[key] = v;
+        ++n_costed;
+        return v;
+      }
+      auto key = std::make_tuple(bp, mask, t);
+      auto it = g.latency_cache.find(key);
+      if (it != g.latency_cache.end()) return it->second;
+      const double v = stage_latency(g, g.ops_of(bp, mask), t, nullptr);
+      ++n_costed;
+      return v;   // stage_latency fills the cache
+    };
+    BlockDP dp(g, bp, r, s, set, fn);
+    std::vector<std::pair<uint64_t, int>> q;
+    const double c = dp.run(&q);
+    total += c;
+    n_states += dp.states();
+    n_trans += dp.transitions();
+    for (auto& [m, t] : q) {
+      Stage st;
+      st.ops = g.ops_of(bp, m);
+      st.strategy = t;
+      st.latency_ms = fn(m, t);
+      out->stages.push_back(st);
+    }
+  }
+  if (stats) {
+    stats[0] = n_states;
+    stats[1] = n_trans;
+    stats[2] = n_costed;
+  }
+  return total;
+}
+
+}  // namespace ios

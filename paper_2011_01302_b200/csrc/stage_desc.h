@@ -1,0 +1,88 @@
+// Device-visible descriptors of one stage plan.
+// Plain structs shared by the host planner (plan.cpp) and the persistent stage kernel
+// (stage_kernel.cu). One stage = one launch; the kernel walks a tile list that spans every
+// member op of the stage ("problems"), in an order where every dependency points backwards.
+#pragma once
+#include <stdint.h>
+
+namespace ios {
+
+// ---- tile geometry -----------------------------------------------------------------------------
+constexpr int kBM = 128;                  // GEMM tile rows (output pixels); UMMA M = 128, cta_group::1
+constexpr int kChunkBytes = 128;          // bytes of K per pipeline stage (32 fp32 / 64 bf16 elements)
+constexpr int kStages = 4;                // smem ring depth
+constexpr int kMaxBN = 256;               // UMMA N <= 256
+constexpr int kAStageBytes = kBM * kChunkBytes;         // 16 KB
+constexpr int kBStageBytes = kMaxBN * kChunkBytes;      // 32 KB
+constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024;  // + barriers/scratch
+constexpr int kProducerWarps = 4;         // warps 0-3: A gather (cp.async) + B bulk copy
+constexpr int kEpilogueWarp0 = 4;         // warps 4-7: TMEM -> registers -> global; SIMT tiles
+constexpr int kMmaWarp = 8;               // warp 8: tcgen05.mma issuer + TMEM allocator
+constexpr int kThreads = 9 * 32;
+constexpr int kTmemCols = 512;            // 2 accumulator buffers x 256 columns
+constexpr int kMaxProblems = 96;
+constexpr int kMaxSegs = 8;               // merged conv: one output segment per branch
+
+enum ProblemKind : int32_t {
+  PK_GEMM = 0,      // implicit-GEMM conv / merged conv / pointwise / linear on tcgen05
+  PK_MAXPOOL = 1,
+  PK_AVGPOOL = 2,
+  PK_GAVGPOOL = 3,
+  PK_ADD = 4,       // sum_i w_i x_i
+  PK_COPY = 5,      // concat (non-elided) / identity: gather input channel ranges into the output
+  PK_DWCONV = 6,    // sepconv front half: ReLU(sum_i w_i x_i) -> depthwise k x k
+};
+
+enum ElemType : int32_t { ET_F32 = 0, ET_BF16 = 1 };
+
+// An NHWC activation view: element (n, h, w, c) at ptr + ((n*H + h)*W + w)*cstride + coff + c.
+// C is the padded channel count (multiple of 8); channels [Cl, C) hold zeros.
+struct View {
+  uint64_t ptr;
+  int32_t cstride, coff, C, Cl, H, W;   // C = padded channels, Cl = logical channels
+};
+
+struct Segment {           // output columns [n0, n1) of a GEMM go to `out` at channel n - n0
+  int32_t n0, n1;
+  View out;
+  int32_t relu, pad_;
+};
+
+struct Problem {
+  int32_t kind, dtype;
+  int32_t tile_begin, n_tiles;      // tiles [tile_begin, tile_begin + n_tiles) of the stage
+  int32_t done_idx;                 // counters[done_idx] += 1 per finished output tile
+  int32_t n_deps;
+  int32_t dep_idx[6];               // wait until counters[dep_idx[i]] >= dep_target[i]
+  int32_t dep_target[6];
+  int32_t batch, flags;             // flags: IOS_F_* of the op
+  int32_t kh, kw, sh, sw, ph, pw;
+  int32_t Ho, Wo;
+  int32_t in_begin, n_in;           // views[in_begin .. in_begin + n_in)
+  View out;                         // SIMT output / GEMM: unused (segments)
+  uint64_t wts;                     // GEMM: packed weights; DWCONV: fp32 [C][kh*kw]
+  uint64_t bias;                    // fp32 [N padded]
+  uint64_t add_w;                   // fp32 [n_in] or 0
+  // GEMM geometry
+  int32_t M, K, k_chunks;           // M = batch*Ho*Wo, K = kh*kw*Cin_p (elements)
+  int32_t BN, n_tiles_n, m_tiles;   // tile = (m, n, split)
+  int32_t split, chunks_per_split;
+  int32_t Npad8;                    // packed weight rows (multiple of 8)
+  int32_t seg_begin, n_seg;
+  uint64_t workspace;               // split-K partials [out tiles][split][kBM][BN] fp32
+  int32_t tilectr_idx;              // split-K arrival counters base
+  // SIMT geometry
+  int32_t items_per_tile, n_items;  // items = output pixels (x channel vectors handled inside)
+  int32_t pad_[2];
+};
+
+struct StageDesc {
+  uint64_t problems;                // Problem[n_problems]
+  uint64_t views;                   // View[]
+  uint64_t segs;                    // Segment[]
+  uint64_t counters;                // int32[n_counters]; [0] = CTA exit counter
+  uint64_t err;                     // int32 error flag (dependency-wait timeout)
+  int32_t n_problems, n_tiles, n_counters, has_gemm;
+};
+
+}  // namespace ios

@@ -1,0 +1,89 @@
+"""GPU parity: the CUDA stage executor (through the C-ABI) vs the oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star; metric DESIGN.md Z13): TF32 5e-3, BF16 2e-2 normwise, per op
+(oracle fed the GPU's own inputs) and end to end.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import OracleGraph, scheduler as S
+from tests.gpu_util import TOL, per_op_errors, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return torch
+
+
+def _run(net, math, schedule="sequential", torch=None, r=3, s=8):
+    from paper_2011_01302_b200 import Graph
+    g = Graph.from_netspec(net, math)
+    if schedule == "sequential":
+        q = g.schedule_sequential()
+    elif schedule == "greedy":
+        q = g.schedule_greedy()
+    else:
+        q = g.schedule(schedule)
+    x = net.make_input()
+    xt = torch.from_numpy(x).cuda()
+    y = g.run(q, xt)
+    torch.cuda.synchronize()
+    return g, q, y.cpu().numpy()
+
+
+@pytest.mark.parametrize("math", ["tf32", "bf16"])
+def test_fig2_sequential_per_op_and_end_to_end(torch_cuda, math):
+    net = W.fig2_block(math=math)
+    g, q, y = _run(net, math, "sequential", torch_cuda)
+    errs = per_op_errors(net, g, math)
+    assert max(errs.values()) < TOL[math], errs
+    ref = OracleGraph(net).run_sequential(net.make_input())[net.n_ops]
+    assert rel_err(y, ref) < TOL[math]
+
+
+@pytest.mark.parametrize("math", ["tf32", "bf16"])
+def test_fig2_every_schedule(torch_cuda, math):
+    """All 44 concurrent-only schedules of the Fig. 2 block plus every merge variant (one launch per
+    stage; chains inside a stage use in-kernel dependency counters) match the oracle."""
+    from paper_2011_01302_b200 import Graph
+    net = W.fig2_block(math=math)
+    og = OracleGraph(net)
+    x = net.make_input()
+    ref = og.run_sequential(x)[og.n]
+    g = Graph.from_netspec(net, math)
+    xt = torch_cuda.from_numpy(x).cuda()
+    mem = og.block_members[0]
+    n = 0
+    for qq in S.all_schedules(og.succ[0], og.pred[0], lambda m: og.mergeable(og.block_mask_ops(0, m))):
+        stages = [([mem[i] for i in range(4) if (m >> i) & 1], t) for m, t in qq] + [([5], 0)]
+        q = g.schedule(stages)
+        y = g.run(q, xt).cpu().numpy()
+        assert rel_err(y, ref) < TOL[math], stages
+        n += 1
+    assert n >= 44
+
+
+@pytest.mark.parametrize("math", ["tf32", "bf16"])
+def test_tiny_mixed_all_op_kinds(torch_cuda, math):
+    net = W.tiny_mixed_net(math=math)
+    for sched in ("sequential", "greedy"):
+        g, q, y = _run(net, math, sched, torch_cuda)
+        errs = per_op_errors(net, g, math)
+        assert max(errs.values()) < TOL[math], (sched, errs)
+        ref = OracleGraph(net).run_sequential(net.make_input())[net.n_ops]
+        assert rel_err(y, ref) < TOL[math]
+
+
+def test_ios_stage_latency_positive(torch_cuda):
+    from paper_2011_01302_b200 import Graph, MERGE
+    net = W.fig2_block()
+    g = Graph.from_netspec(net)
+    t1 = g.stage_latency([1])
+    t_all = g.stage_latency([1, 2, 3, 4])
+    t_m = g.stage_latency([1, 3, 4], MERGE)
+    assert 0 < t1 < 1.0 and 0 < t_all < 1.0 and 0 < t_m < 1.0
