@@ -1,0 +1,350 @@
+"""Benchmark of the IOS stage executor (BASELINE.json metric: batch-1 latency ms of the IOS schedule
+vs the sequential and greedy schedules on the same kernels, + % of per-stage roofline).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--net inception_v3] [--impl ours|reference]
+
+One step = one batch-1 inference of the whole network through ios_run (every stage of Q, one
+launch each, captured in a CUDA graph), inputs resident in HBM; L2 is flushed (a 2x-L2 write)
+before every timed step. N > 1: one process per GPU (torchrun), replicas only (batch 1 does not
+shard), device time max over ranks. `--impl reference` times the CPU oracle
+(the tier's reference arm) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NETS = {
+    "inception_v3": dict(math="tf32", desc="Inception V3 batch 1, 299x299, TF32 on 1xB200"),
+    "nasnet_a_large": dict(math="tf32", desc="NasNet-A large batch 1, 331x331, TF32"),
+    "randwire_ws_small": dict(math="bf16", desc="RandWire-WS small batch 1, 224x224, BF16"),
+    "squeezenet": dict(math="tf32", desc="SqueezeNet v1.0 224x224, TF32"),
+    "fig2": dict(math="tf32", desc="Fig.2 4-conv block 1x64x28x28, TF32"),
+}
+METRIC = "batch-1 latency ms (IOS vs sequential/greedy schedule) + % stage roofline"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    src = "measured"
+    try:
+        m = json.load(open(p))
+        hbm, bf16 = float(m["hbm_gbs"]), float(m["bf16_tflops"])
+    except Exception:
+        hbm, bf16, src = 6650.0, 1590.0, "fallback"
+    # TF32 has no measured peak: the measured bf16 burst x the guide's nominal tf32/bf16 ratio (1.1/2.25)
+    return {"hbm_gbs": hbm, "bf16_tflops": bf16, "tf32_tflops": bf16 * 1.1 / 2.25, "source": src}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/ios_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def stage_roofline(g, net, q, peaks):
+    """Per-stage roofline: T_roof = max(F / P_tc, B / BW_HBM) with F = unpadded conv
+    FLOPs and B = distinct input bytes + weight bytes + output bytes (elided concat = 0)."""
+    from workloads.netspec import NetSpec  # noqa: F401
+    esz = 2 if net.math == "bf16" else 4
+    ptc = (peaks["bf16_tflops"] if net.math == "bf16" else peaks["tf32_tflops"]) * 1e12
+    bw = peaks["hbm_gbs"] * 1e9
+    shapes = {i: g.op_shape(i) for i in range(net.n_ops + 1)}
+    rows = []
+    for ops, t, lat in q.stages:
+        f = 0
+        wbytes = 0
+        in_ids = set()
+        out_b = 0
+        for v in ops:
+            o = net.op(v)
+            n, co, ho, wo = shapes[v]
+            if o.kind == "conv":
+                cin = shapes[o.inputs[0]][1]
+                f += 2 * n * ho * wo * co * cin * o.kh * o.kw
+                wbytes += co * cin * o.kh * o.kw * esz
+            elif o.kind == "sepconv":
+                c = shapes[o.inputs[0]][1]
+                f += 2 * n * ho * wo * c * (o.kh * o.kw + co)
+                wbytes += (c * o.kh * o.kw + co * c) * esz
+            elif o.kind == "linear":
+                cin = shapes[o.inputs[0]][1]
+                f += 2 * n * co * cin
+                wbytes += co * cin * esz
+            if o.kind != "concat" and o.kind != "identity":
+                out_b += n * co * ho * wo * esz
+                for u in o.inputs:
+                    if u not in ops:
+                        in_ids.add(u)
+        in_b = sum(shapes[u][0] * shapes[u][1] * shapes[u][2] * shapes[u][3] * esz for u in in_ids)
+        b = in_b + wbytes + out_b
+        t_roof = max(f / ptc, b / bw) * 1e3
+        rows.append({"ops": ops, "strategy": t, "ms": lat, "flops": f, "bytes": b, "roof_ms": t_roof,
+                     "bound": "tensor" if f / ptc >= b / bw else "hbm"})
+    return rows
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import workloads as W
+    from paper_2011_01302_b200 import Graph
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    spec = NETS[args.net]
+    net = W.build(args.net, math=spec["math"])
+    peaks = _peaks()
+
+    g = Graph.from_netspec(net, spec["math"], local)
+    t0 = time.time()
+    q_ios = g.schedule_dp(args.r, args.s)                      # device-measured stage costs (Alg. 1)
+    search_s = time.time() - t0
+    q_seq = g.schedule_sequential()
+    q_greedy = g.schedule_greedy()
+
+    x = torch.from_numpy(net.make_input()).to(dev)
+    out = torch.empty(g.output_shape(), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(int(2 * torch.cuda.get_device_properties(dev).L2_cache_size) // 4 + 1024,
+                        dtype=torch.float32, device=dev)
+
+    def timed(q, steps, warmup, sampler=None):
+        for _ in range(warmup):
+            g.run(q, x, out)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda.synchronize(dev)
+        for i in range(steps):
+            flush.fill_(float(i))                              # L2 flush between timed steps (untimed)
+            evs[i][0].record(stream)
+            g.run(q, x, out)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        tot = sum(a.elapsed_time(b) for a, b in evs)
+        t = torch.tensor([tot / steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(local) as clk:
+        ms_ios = timed(q_ios, args.steps, args.warmup)
+    ms_seq = timed(q_seq, max(20, args.steps // 4), args.warmup)
+    ms_greedy = timed(q_greedy, max(20, args.steps // 4), args.warmup)
+
+    # end to end through the public API with HOST buffers (pinned input copy in, output copy out)
+    xh = torch.from_numpy(net.make_input()).pin_memory()
+    yh = torch.empty(g.output_shape(), dtype=torch.float32).pin_memory()
+    for _ in range(args.warmup):
+        x.copy_(xh, non_blocking=True)
+        g.run(q_ios, x, out)
+        yh.copy_(out, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(20, args.steps // 4)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        x.copy_(xh, non_blocking=True)
+        g.run(q_ios, x, out)
+        yh.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+
+    # per-stage roofline of the IOS schedule: stage latencies are CUDA-event timings of each stage
+    # launch alone (the profiler that fed the DP; ios_stage_latency)
+    rows = stage_roofline(g, net, q_ios, peaks)
+    launches_per_run = q_ios.launches()
+    if rank == 0:
+        tot_roof = sum(r["roof_ms"] for r in rows)
+        tot_ms = sum(r["ms"] for r in rows if r["ms"] > 0)
+        conv_rows = [r for r in rows if r["roof_ms"] >= 0.002 and r["flops"] > 0]
+        f_tot = sum(r["flops"] for r in rows)
+        b_tot = sum(r["bytes"] for r in rows)
+        tc_time = sum(r["flops"] for r in rows) / ((peaks["bf16_tflops"] if net.math == "bf16" else peaks["tf32_tflops"]) * 1e9)
+        hbm_time = b_tot / (peaks["hbm_gbs"] * 1e6)
+        bound = "tensor" if tc_time >= hbm_time else "hbm"
+        if bound == "tensor":
+            achieved = f_tot / (tot_ms * 1e9)            # TFLOP/s
+            peak = peaks["bf16_tflops"] if net.math == "bf16" else peaks["tf32_tflops"]
+            unit = "TFLOP/s"
+        else:
+            achieved = b_tot / (tot_ms * 1e6)            # GB/s
+            peak = peaks["hbm_gbs"]
+            unit = "GB/s"
+        cpu = cpu_baseline(net, args.cpu_sample_s)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"traffic_{args.net}.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("bytes_per_step")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC,
+            "value": round(ms_ios, 4),
+            "unit": "ms",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_ios, 4),
+            "higher_is_better": False,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16" if net.math == "bf16" else "tf32",
+            "data": "synthetic (seeded N(0,1) input, He-init weights, DESIGN.md input recipe)",
+            "config": {"workload": spec["desc"], "net": args.net, "batch": 1, "schedule": f"IOS-Both r={args.r} s={args.s}",
+                       "parallelism": f"replicas x{world} (batch 1 does not shard)", "l2": "flushed before every timed step",
+                       "stages": len(q_ios.stages), "launches_per_run": launches_per_run},
+            "sequential_ms": round(ms_seq, 4),
+            "greedy_ms": round(ms_greedy, 4),
+            "speedup_vs_sequential": round(ms_seq / ms_ios, 3),
+            "speedup_vs_greedy": round(ms_greedy / ms_ios, 3),
+            "images_per_s": round(world * 1000.0 / ms_ios, 1),
+            "search_s": round(search_s, 2),
+            "search_stats": {"states": q_ios.stats[0], "transitions": q_ios.stats[1], "stages_measured": q_ios.stats[2]},
+            "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": unit,
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": peaks["source"] + (" (tf32 = bf16 x 1.1/2.25 nominal)" if net.math != "bf16" else ""),
+                         "kernel": "ios_stage_kernel (all stages; per-stage CUDA-event durations)"},
+            "stage_roofline": {"frac_sum": round(tot_roof / tot_ms, 4) if tot_ms else None,
+                               "conv_stages": len(conv_rows),
+                               "conv_stages_ge_50pct": sum(1 for r in conv_rows if r["ms"] > 0 and r["roof_ms"] / r["ms"] >= 0.5),
+                               "roof_ms_sum": round(tot_roof, 4), "stage_ms_sum": round(tot_ms, 4)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(float(e2e_ms.item()), 4), "unit": "ms",
+                    "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4)},
+            "gpu_launches": int(launches_per_run * args.steps),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(net, budget_s: float):
+    """The oracle as it stands (plain NumPy float64 sequential executor), timed on this host."""
+    from oracle import OracleGraph
+    try:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(limits=1)
+    except Exception:
+        ctx = None
+    og = OracleGraph(net)
+    x = net.make_input()
+    times = []
+    t_start = time.time()
+    while not times or (time.time() - t_start < budget_s and len(times) < 3):
+        t0 = time.perf_counter()
+        og.run_sequential(x)
+        times.append(time.perf_counter() - t0)
+    if ctx is not None:
+        ctx.unregister() if hasattr(ctx, "unregister") else None
+    ms = sorted(times)[len(times) // 2] * 1e3
+    return {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": "oracle",
+            "sample": f"{len(times)} full batch-1 inference(s) of the same network (run_sequential, float64)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as it stands (the tier's reference arm)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import workloads as W
+    from oracle import OracleGraph
+    spec = NETS[args.net]
+    net = W.build(args.net, math=spec["math"])
+    og = OracleGraph(net)
+    x = net.make_input()
+    for _ in range(min(args.warmup, 1)):
+        og.run_sequential(x)
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        og.run_sequential(x)
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    line = {"impl": "reference", "metric": METRIC, "value": round(ms, 2), "unit": "ms", "n_gpus": world,
+            "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": round(ms, 2), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": spec["desc"], "net": args.net, "batch": 1, "schedule": "sequential (oracle)"},
+            "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": "oracle",
+                             "sample": f"{steps} full batch-1 inference(s), float64 NumPy"},
+            "e2e": {"value": round(ms, 2), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--net", default="inception_v3", choices=sorted(NETS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--r", type=int, default=3)
+    ap.add_argument("--s", type=int, default=8)
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -36,6 +36,7 @@ struct OpDev {
 struct StagePlan {
   StageDesc sd{};
   int grid = 0;
+  int dtype = 0;
   bool empty = true;
   void* dmem = nullptr;       // problems | views | segments
   int* counters = nullptr;
@@ -554,6 +555,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       sd.has_gemm = 0;
       for (Problem& p : b.probs) sd.has_gemm |= p.kind == PK_GEMM;
       plan->grid = std::min(tiles, d.num_sms);
+      plan->dtype = g.dtype();
     }
   } catch (...) {
     delete plan;
@@ -574,7 +576,7 @@ StagePlan* get_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
 
 void launch_plan(const StagePlan* p, cudaStream_t st) {
   if (p->empty) return;
-  IOS_CHECK_CUDA(launch_stage(p->sd, p->grid, st));
+  IOS_CHECK_CUDA(launch_stage(p->sd, p->dtype, p->grid, st));
 }
 
 void check_err(DeviceState& d) {
@@ -648,7 +650,7 @@ void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStre
     for (StagePlan* p : plans) {
       if (e != cudaSuccess) break;
       if (p->empty) continue;
-      e = launch_stage(p->sd, p->grid, d.stream);
+      e = launch_stage(p->sd, p->dtype, p->grid, d.stream);
       ++launches;
     }
     if (e == cudaSuccess) {

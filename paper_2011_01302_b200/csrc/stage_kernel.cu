@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "stage_desc.h"
 
@@ -64,6 +65,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) {
+  __syncwarp();   // bar.sync is .aligned: reconverge lanes that diverged (e.g. one lane spun on a counter)
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -87,8 +89,9 @@ __device__ __forceinline__ uint32_t umma_idesc(int bf16, int n) {
   const uint32_t f = bf16 ? 1u : 2u;
   return (1u << 4) | (f << 7) | (f << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 }
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc, int bf16) {
-  if (bf16)
+template <int DT>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (DT == ET_BF16)
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
@@ -101,10 +104,18 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, ui
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 r;\n\t.reg .pred p;\n\telect.sync r|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  __syncwarp();   // tcgen05.ld is .sync.aligned
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
@@ -347,6 +358,7 @@ __device__ __forceinline__ int find_problem(const int* sm_tile_begin, int n_prob
   return p;
 }
 
+template <int DT>
 __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc sd) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -382,6 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp && sd.has_gemm) {
+    __syncwarp();
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(kTmemCols)
                  : "memory");
@@ -436,7 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         rbase[j] = (int64_t)n * in.H * in.W;
       }
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts);
-      const uint32_t bbytes = (uint32_t)P.BN * kChunkBytes;
+      // the last n tile may run past the packed rows: copy only those (the rest of the smem tile is
+      // stale and only feeds accumulator columns that no output segment covers)
+      const uint32_t bbytes = (uint32_t)min(P.BN, P.Npad8 - nt * P.BN) * kChunkBytes;
       int pend[2] = {-1, -1};
       for (int c = c0; c < c1; ++c) {
         mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
@@ -497,8 +512,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       if (pend[1] >= 0) mbar_arrive(smem_u32(&full[pend[1]]));
     }
   } else if (warp == kMmaWarp) {
-    // ============================================================== MMA ISSUER (one thread)
-    if (lane == 0 && sd.has_gemm) {
+    // ============================================================== MMA ISSUER
+    // The whole warp walks the tiles and waits on the barriers (warp-uniform control flow); one
+    // elected lane issues tcgen05.mma / tcgen05.commit.
+    if (sd.has_gemm) {
       Ring ring;
       int acc = 0;
       uint32_t acc_phase = 0;
@@ -511,8 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const int s = local % P.split;
         const int c0 = s * P.chunks_per_split;
         const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
-        const int bf16 = P.dtype == ET_BF16;
-        const uint32_t idesc = umma_idesc(bf16, P.BN);
+        const uint32_t idesc = umma_idesc(DT == ET_BF16, P.BN);
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)acc * kMaxBN;
@@ -521,15 +537,19 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + ring.slot * kAStageBytes);
           const uint32_t b0 = smem_u32(sB + ring.slot * kBStageBytes);
+          __syncwarp();
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {   // 4 x 32 B of K per 128 B chunk
-            umma(tmem_d, umma_desc(a0 + kk * 256, 128, 1024), umma_desc(b0 + kk * 256, 128, 1024), idesc,
-                 (c > c0 || kk > 0) ? 1u : 0u, bf16);
+            for (int kk = 0; kk < 4; ++kk)   // 4 x 32 B of K per 128 B chunk
+              umma<DT>(tmem_d, umma_desc(a0 + kk * 256, 128, 1024), umma_desc(b0 + kk * 256, 128, 1024), idesc,
+                       (c > c0 || kk > 0) ? 1u : 0u);
+            umma_commit(smem_u32(&empty[ring.slot]));
           }
-          umma_commit(smem_u32(&empty[ring.slot]));
+          __syncwarp();
           ring.next();
         }
-        umma_commit(smem_u32(&tfull[acc]));
+        if (elect_one()) umma_commit(smem_u32(&tfull[acc]));
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1u;
       }
@@ -674,6 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   }
 
   // ---------------------------------------------------------------------------- teardown
+  __syncwarp();   // the MMA warp ran its loop on lane 0 only
   tc_fence_before();
   __syncthreads();
   if (warp == kMmaWarp && sd.has_gemm) {
@@ -726,14 +747,19 @@ __global__ void l2_flush_kernel(int4* buf, int64_t n) {
 }
 
 // ------------------------------------------------------------------------------ host launchers
-cudaError_t launch_stage(const StageDesc& sd, int grid, cudaStream_t st) {
+cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(ios_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
+    cudaError_t e = cudaFuncSetAttribute(ios_stage_kernel<ET_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ios_stage_kernel<ET_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  ios_stage_kernel<<<grid, kThreads, kSmemBytes + 1024, st>>>(sd);
+  if (dtype == ET_BF16)
+    ios_stage_kernel<ET_BF16><<<grid, kThreads, kSmemBytes + 1024, st>>>(sd);
+  else
+    ios_stage_kernel<ET_F32><<<grid, kThreads, kSmemBytes + 1024, st>>>(sd);
   return cudaGetLastError();
 }
 
