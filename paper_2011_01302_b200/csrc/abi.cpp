@@ -496,6 +496,16 @@ ios_status ios_latency_cache_load(ios_graph gh, const char* path) {
   ABI_END
 }
 
+ios_status ios_stage_trace(ios_graph gh, const int32_t* ops, int32_t n, ios_strategy t, uint64_t* out, int32_t cap,
+                           int32_t* grid) {
+  ABI_BEGIN
+  REQUIRE(gh && ops && out && grid && n >= 1, "bad arguments");
+  std::vector<int> v(ops, ops + n);
+  std::sort(v.begin(), v.end());
+  *grid = stage_trace(gh->g, v, t, out, cap);
+  ABI_END
+}
+
 void ios_schedule_destroy(ios_schedule q) { delete q; }
 void ios_graph_destroy(ios_graph g) { delete g; }
 

@@ -251,7 +251,9 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
     GemmSpec* best = nullptr;
     double best_cost = 0;
     for (GemmSpec* p : gs) {
-      const bool can_n = p->BN >= 128;
+      // small-M GEMMs are weight-bound: narrow N tiles first (A is small and L2-resident), then split K
+      const int min_bn = p->mt <= 2 ? 16 : 64;
+      const bool can_n = p->BN >= 2 * min_bn;
       const bool can_k = p->cps >= 4 && p->split < 32;
       if (!can_n && !can_k) continue;
       const double c = p->cps * (1.0 + p->BN / 256.0);
@@ -261,7 +263,7 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       }
     }
     if (!best) break;
-    if (best->BN >= 128) {
+    if (best->BN >= 2 * (best->mt <= 2 ? 16 : 64)) {
       best->BN = round_up(best->BN / 2, 16);
       best->ntn = (best->N16 + best->BN - 1) / best->BN;
     } else {
@@ -480,10 +482,11 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       const int nvec = p.out.C / nv;
       if (p.kind == PK_GAVGPOOL) {
         p.n_items = p.batch * nvec;
-        p.items_per_tile = 128;
+        p.items_per_tile = 32;
       } else {
+        // about 4 vector items per epilogue thread so the stage spreads over many SMs
         p.n_items = p.batch * p.Ho * p.Wo;
-        p.items_per_tile = std::max(1, 2048 / std::max(1, nvec));
+        p.items_per_tile = std::max(1, 256 / std::max(1, nvec));
       }
       p.n_tiles = (p.n_items + p.items_per_tile - 1) / p.items_per_tile;
       simt_tiles += p.n_tiles;
@@ -498,6 +501,13 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       Problem& p = b.probs[i];
       if (p.kind != PK_GEMM) continue;
       const GemmSpec& s = b.specs[i];
+      const View& in = b.views[p.in_begin];
+      p.fd_howo = make_fastdiv((uint32_t)(p.Ho * p.Wo));
+      p.fd_wo = make_fastdiv((uint32_t)p.Wo);
+      p.fd_split = make_fastdiv((uint32_t)s.split);
+      p.fd_ntn = make_fastdiv((uint32_t)s.ntn);
+      p.fd_cin = make_fastdiv((uint32_t)in.C);
+      p.fd_kw = make_fastdiv((uint32_t)p.kw);
       p.BN = s.BN;
       p.n_tiles_n = s.ntn;
       p.m_tiles = s.mt;
@@ -537,6 +547,9 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
         if (p.kind == PK_GEMM && p.split > 1) p.workspace += (uint64_t)plan->workspace;
       const size_t pb = b.probs.size() * sizeof(Problem), vb = b.views.size() * sizeof(View),
                    sb = b.segs.size() * sizeof(Segment);
+      // a problem signals completion only if a later member of the stage waits on it
+      for (Problem& p : b.probs)
+        for (int k = 0; k < p.n_deps; ++k) b.probs[p.dep_idx[k] - 1].signal = 1;
       std::vector<uint8_t> blob(pb + vb + sb + 64, 0);
       std::memcpy(blob.data(), b.probs.data(), pb);
       if (vb) std::memcpy(blob.data() + pb, b.views.data(), vb);
@@ -552,6 +565,9 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       sd.n_problems = np;
       sd.n_tiles = tiles;
       sd.n_counters = n_counters;
+      sd.blob_bytes = (int)(pb + vb + sb);
+      sd.views_off = (int)pb;
+      sd.segs_off = (int)(pb + vb);
       sd.has_gemm = 0;
       for (Problem& p : b.probs) sd.has_gemm |= p.kind == PK_GEMM;
       plan->grid = std::min(tiles, d.num_sms);
@@ -628,6 +644,26 @@ double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const 
   }
   g.latency_cache[std::make_tuple(bpos, mask, strategy)] = ms;
   return ms;
+}
+
+int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* out, int cap) {
+  ensure_device(g);
+  DeviceState& d = *g.dev;
+  int bpos = -1;
+  const uint64_t mask = g.mask_of(ops, &bpos);
+  StagePlan* p = get_plan(g, bpos, mask, strategy);
+  if (p->empty) return 0;
+  launch_plan(p, d.stream);                        // warm
+  const size_t n = (size_t)p->grid * 16;
+  uint64_t* buf = static_cast<uint64_t*>(dmalloc(d, n * sizeof(uint64_t)));
+  StageDesc sd = p->sd;
+  sd.trace = (uint64_t)buf;
+  IOS_CHECK_CUDA(launch_stage(sd, p->dtype, p->grid, d.stream));
+  IOS_CHECK_CUDA(cudaStreamSynchronize(d.stream));
+  std::vector<uint64_t> h(n);
+  IOS_CHECK_CUDA(cudaMemcpy(h.data(), buf, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n && i < (size_t)cap; ++i) out[i] = h[i];
+  return p->grid;
 }
 
 void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStream_t st) {

@@ -157,7 +157,10 @@ double schedule_dp(Graph& g, int r, int s, int set, ios_cost_fn cost, void* ctx,
       auto key = std::make_tuple(bp, mask, t);
       auto it = g.latency_cache.find(key);
       if (it != g.latency_cache.end()) return it->second;
-      const double v = stage_latency(g, g.ops_of(bp, mask), t, nullptr);
+      // search-time profile: fewer repetitions than ios_stage_latency's defaults (Z15); the DP
+      // needs a ranking of stages, and every (block, mask, T) is measured once and cached
+      static const ios_profile_opts search_opts{3, 3, 8, 0};
+      const double v = stage_latency(g, g.ops_of(bp, mask), t, &search_opts);
       ++n_costed;
       return v;   // stage_latency fills the cache
     };

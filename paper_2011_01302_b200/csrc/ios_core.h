@@ -101,6 +101,7 @@ double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const 
 void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStream_t st);
 void op_output(Graph& g, int op, void* d_out, cudaStream_t st);
 int schedule_launches(Graph& g, Schedule& q);
+int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* out, int cap);
 void destroy_device(Graph& g);
 void destroy_schedule_exec(Schedule& q);
 

@@ -14,7 +14,10 @@ constexpr int kStages = 4;                // smem ring depth
 constexpr int kMaxBN = 256;               // UMMA N <= 256
 constexpr int kAStageBytes = kBM * kChunkBytes;         // 16 KB
 constexpr int kBStageBytes = kMaxBN * kChunkBytes;      // 32 KB
-constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024;  // + barriers/scratch
+constexpr int kBarBytes = 256;            // mbarriers, TMEM slot, flags
+constexpr int kBiasBytes = 2 * kMaxBN * 4; // bias slice per accumulator buffer
+constexpr int kDescBytes = 26 * 1024;     // stage descriptor table (problems | views | segments) copy
+constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + kBarBytes + kBiasBytes + kDescBytes;
 constexpr int kProducerWarps = 4;         // warps 0-3: A gather (cp.async) + B bulk copy
 constexpr int kEpilogueWarp0 = 4;         // warps 4-7: TMEM -> registers -> global; SIMT tiles
 constexpr int kMmaWarp = 8;               // warp 8: tcgen05.mma issuer + TMEM allocator
@@ -48,6 +51,17 @@ struct Segment {           // output columns [n0, n1) of a GEMM go to `out` at c
   int32_t relu, pad_;
 };
 
+// x / d for 0 <= x < 2^31 with one multiply-high (round-up multiplier method); built on the host.
+struct FastDiv {
+  uint32_t d, mul, shift, pad_;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t sh = 0;
+  while ((1ull << sh) < d) ++sh;
+  const uint64_t mul = ((1ull << 32) * ((1ull << sh) - d)) / d + 1;
+  return FastDiv{d, (uint32_t)mul, sh, 0};
+}
+
 struct Problem {
   int32_t kind, dtype;
   int32_t tile_begin, n_tiles;      // tiles [tile_begin, tile_begin + n_tiles) of the stage
@@ -71,9 +85,11 @@ struct Problem {
   int32_t seg_begin, n_seg;
   uint64_t workspace;               // split-K partials [out tiles][split][kBM][BN] fp32
   int32_t tilectr_idx;              // split-K arrival counters base
+  int32_t signal;                   // 1: a later member of the stage waits on done_idx
+  FastDiv fd_howo, fd_wo, fd_split, fd_ntn, fd_cin, fd_kw;   // divisors of the tile / im2col decode
   // SIMT geometry
   int32_t items_per_tile, n_items;  // items = output pixels (x channel vectors handled inside)
-  int32_t pad_[2];
+  int32_t pad_[1];
 };
 
 struct StageDesc {
@@ -82,7 +98,10 @@ struct StageDesc {
   uint64_t segs;                    // Segment[]
   uint64_t counters;                // int32[n_counters]; [0] = CTA exit counter
   uint64_t err;                     // int32 error flag (dependency-wait timeout)
+  uint64_t trace;                   // optional uint64 [grid][16] timeline (0 = off)
   int32_t n_problems, n_tiles, n_counters, has_gemm;
+  int32_t blob_bytes;               // problems | views | segments, contiguous from `problems`
+  int32_t views_off, segs_off, pad_;
 };
 
 }  // namespace ios

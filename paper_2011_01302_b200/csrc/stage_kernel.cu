@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <climits>
 #include <cstdio>
 
 #include "stage_desc.h"
@@ -56,6 +57,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool zero) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "cp.async.cg.shared.global [%0], [%1], 16, p;\n\t}" ::"r"(dst),
+      "l"(src), "r"((int)zero)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -67,6 +75,14 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void named_bar(int id, int n) {
   __syncwarp();   // bar.sync is .aligned: reconverge lanes that diverged (e.g. one lane spun on a counter)
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ int fdiv(const FastDiv& f, int x) {
+  return (int)((__umulhi((uint32_t)x, f.mul) + (uint32_t)x) >> f.shift);
+}
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -114,7 +130,7 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
   __syncwarp();   // tcgen05.ld is .sync.aligned
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -199,146 +215,150 @@ __device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* 
 }
 
 // -------------------------------------------------------------------------------- SIMT tile body
-// Runs on the 128 epilogue threads. Items are output pixels x 16 B channel vectors.
-__device__ void simt_tile(const Problem& P, const View* views, int tile, int tid) {
-  const int dtype = P.dtype;
-  const int nv = dtype == ET_F32 ? 4 : 8;
+// Memory-bound members. Items are (output pixel, 16 B channel vector); consecutive
+// threads take consecutive vectors of one pixel (coalesced). Code size matters as much as ILP
+// here: the whole stage kernel shares one instruction cache, so this body is one __noinline__
+// function with short, register-resident loops (3-wide window rows: 3 loads in flight per row).
+template <int DT>
+__device__ __forceinline__ void ld16(const View& vw, int64_t pix, int c, float* out) {
+  load_vec(vw, DT, pix, c, out, DT == ET_BF16 ? 8 : 4);
+}
+
+template <int DT>
+__device__ __noinline__ void simt_tile(const Problem& P, const View* views, int tile, int tid, int nthr) {
+  constexpr int NV = DT == ET_BF16 ? 8 : 4;
   const View& out = P.out;
-  const int nvec = out.C / nv;
+  const int nvec = out.C / NV;
   const int item0 = tile * P.items_per_tile;
   const int item1 = min(item0 + P.items_per_tile, P.n_items);
   if (P.kind == PK_GAVGPOOL) {
-    // items = (image, channel vector); reduce over H*W
     const View& in = views[P.in_begin];
     const int hw = in.H * in.W;
     const float inv = 1.0f / (float)hw;
-    for (int idx = item0 + tid; idx < item1; idx += 128) {
+    const bool relu = (P.flags & 2) != 0;
+    for (int idx = item0 + tid; idx < item1; idx += nthr) {
       const int n = idx / nvec, v = idx % nvec;
       float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int p = 0; p < hw; ++p) {
-        float x[8];
-        load_vec(in, dtype, (int64_t)n * hw + p, v * nv, x, nv);
+      for (int p0 = 0; p0 < hw; p0 += 4) {
+        float x0[8], x1[8], x2[8], x3[8];
+        const int64_t b = (int64_t)n * hw + p0;
+        ld16<DT>(in, b, v * NV, x0);
+        if (p0 + 1 < hw) ld16<DT>(in, b + 1, v * NV, x1);
+        if (p0 + 2 < hw) ld16<DT>(in, b + 2, v * NV, x2);
+        if (p0 + 3 < hw) ld16<DT>(in, b + 3, v * NV, x3);
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (e < nv) acc[e] += (P.flags & 2) ? fmaxf(x[e], 0.f) : x[e];
+        for (int e = 0; e < NV; ++e) {
+          acc[e] += relu ? fmaxf(x0[e], 0.f) : x0[e];
+          if (p0 + 1 < hw) acc[e] += relu ? fmaxf(x1[e], 0.f) : x1[e];
+          if (p0 + 2 < hw) acc[e] += relu ? fmaxf(x2[e], 0.f) : x2[e];
+          if (p0 + 3 < hw) acc[e] += relu ? fmaxf(x3[e], 0.f) : x3[e];
+        }
       }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] *= inv;
-      store_vec(out, dtype, n, v * nv, acc);
+      for (int e = 0; e < NV; ++e) acc[e] *= inv;
+      store_vec(out, DT, n, v * NV, acc);
     }
     return;
   }
   const int total = (item1 - item0) * nvec;
   const int HoWo = P.Ho * P.Wo;
-  for (int idx = tid; idx < total; idx += 128) {
+  const float* aw = reinterpret_cast<const float*>(P.add_w);
+  for (int idx = tid; idx < total; idx += nthr) {
     const int pix = item0 + idx / nvec;       // output pixel (n, oh, ow)
-    const int c = (idx % nvec) * nv;
+    const int c = (idx % nvec) * NV;
     const int n = pix / HoWo;
     const int rem = pix - n * HoWo;
     const int oh = rem / P.Wo, ow = rem - (rem / P.Wo) * P.Wo;
-    float acc[8];
-    switch (P.kind) {
-      case PK_ADD: {
-        const float* aw = reinterpret_cast<const float*>(P.add_w);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (P.kind == PK_ADD) {
+      for (int i = 0; i < P.n_in; ++i) {
+        float x[8];
+        ld16<DT>(views[P.in_begin + i], pix, c, x);
+        const float w = aw ? aw[i] : 1.0f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+        for (int e = 0; e < NV; ++e) acc[e] = fmaf(w, x[e], acc[e]);
+      }
+    } else if (P.kind == PK_MAXPOOL || P.kind == PK_AVGPOOL || P.kind == PK_DWCONV) {
+      // window rows; three taps of a row are loaded before use
+      const View& in = views[P.in_begin];
+      const bool is_max = P.kind == PK_MAXPOOL, is_dw = P.kind == PK_DWCONV;
+      if (is_max) {
+#pragma unroll
+        for (int e = 0; e < NV; ++e) acc[e] = -INFINITY;
+      }
+      const float* wd = reinterpret_cast<const float*>(P.wts);
+      const int hs = oh * P.sh - P.ph, ws = ow * P.sw - P.pw;
+      const int nin = is_dw ? P.n_in : 1;
+      for (int i = 0; i < P.kh; ++i) {
+        const int ih = hs + i;
+        if (ih < 0 || ih >= in.H) continue;
+        const int64_t rowpix = ((int64_t)n * in.H + ih) * in.W;
+        for (int j0 = 0; j0 < P.kw; j0 += 3) {
+          float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          const int iw = ws + j0;
+          const bool v0 = iw >= 0 && iw < in.W;
+          const bool v1 = j0 + 1 < P.kw && iw + 1 >= 0 && iw + 1 < in.W;
+          const bool v2 = j0 + 2 < P.kw && iw + 2 >= 0 && iw + 2 < in.W;
+          for (int s = 0; s < nin; ++s) {     // sepconv: weighted sum of its inputs
+            const View& vs = views[P.in_begin + s];
+            const float w = (is_dw && aw) ? aw[s] : 1.0f;
+            float x0[8], x1[8], x2[8];
+            if (v0) ld16<DT>(vs, rowpix + iw, c, x0);
+            if (v1) ld16<DT>(vs, rowpix + iw + 1, c, x1);
+            if (v2) ld16<DT>(vs, rowpix + iw + 2, c, x2);
+#pragma unroll
+            for (int e = 0; e < NV; ++e) {
+              if (v0) a0[e] = fmaf(w, x0[e], a0[e]);
+              if (v1) a1[e] = fmaf(w, x1[e], a1[e]);
+              if (v2) a2[e] = fmaf(w, x2[e], a2[e]);
+            }
+          }
+          if (is_dw) {
+            const int kk = P.kh * P.kw, tap = i * P.kw + j0;
+#pragma unroll
+            for (int e = 0; e < NV; ++e) {
+              const float* we = wd + (c + e) * kk + tap;
+              if (v0) acc[e] = fmaf(__ldg(we), fmaxf(a0[e], 0.f), acc[e]);
+              if (v1) acc[e] = fmaf(__ldg(we + 1), fmaxf(a1[e], 0.f), acc[e]);
+              if (v2) acc[e] = fmaf(__ldg(we + 2), fmaxf(a2[e], 0.f), acc[e]);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < NV; ++e) {
+              if (v0) acc[e] = is_max ? fmaxf(acc[e], a0[e]) : acc[e] + a0[e];
+              if (v1) acc[e] = is_max ? fmaxf(acc[e], a1[e]) : acc[e] + a1[e];
+              if (v2) acc[e] = is_max ? fmaxf(acc[e], a2[e]) : acc[e] + a2[e];
+            }
+          }
+        }
+      }
+      if (P.kind == PK_AVGPOOL) {
+        // divisor: window clipped to the padded input (include pad) or to the input (exclude pad)
+        const int he = min(hs + P.kh, in.H + P.ph), we = min(ws + P.kw, in.W + P.pw);
+        int div;
+        if (P.flags & 8) div = (he - hs) * (we - ws);
+        else div = (min(he, in.H) - max(hs, 0)) * (min(we, in.W) - max(ws, 0));
+        const float inv = 1.0f / (float)div;
+#pragma unroll
+        for (int e = 0; e < NV; ++e) acc[e] *= inv;
+      }
+    } else {
+      // PK_COPY: concat gather, element-wise (inputs may have non-vector channel counts)
+      for (int e = 0; e < NV; ++e) {
+        int ch = c + e, off = 0;
         for (int i = 0; i < P.n_in; ++i) {
-          float x[8];
-          load_vec(views[P.in_begin + i], dtype, pix, c, x, nv);
-          const float w = aw ? aw[i] : 1.0f;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] = fmaf(w, x[e], acc[e]);
-        }
-        break;
-      }
-      case PK_MAXPOOL:
-      case PK_AVGPOOL: {
-        const View& in = views[P.in_begin];
-        const bool is_max = P.kind == PK_MAXPOOL;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = is_max ? -INFINITY : 0.f;
-        const int hs = oh * P.sh - P.ph, ws = ow * P.sw - P.pw;
-        for (int i = 0; i < P.kh; ++i) {
-          const int ih = hs + i;
-          if (ih < 0 || ih >= in.H) continue;
-          for (int j = 0; j < P.kw; ++j) {
-            const int iw = ws + j;
-            if (iw < 0 || iw >= in.W) continue;
-            float x[8];
-            load_vec(in, dtype, ((int64_t)n * in.H + ih) * in.W + iw, c, x, nv);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] = is_max ? fmaxf(acc[e], x[e]) : acc[e] + x[e];
+          const View& vi = views[P.in_begin + i];
+          if (ch < off + vi.Cl) {
+            acc[e] = load_elem(vi, DT, pix, ch - off);
+            break;
           }
+          off += vi.Cl;
         }
-        if (!is_max) {
-          // divisor: window clipped to the padded input (include pad) or to the input (exclude pad)
-          const int he = min(hs + P.kh, in.H + P.ph), we = min(ws + P.kw, in.W + P.pw);
-          int div;
-          if (P.flags & 8) div = (he - hs) * (we - ws);
-          else div = (min(he, in.H) - max(hs, 0)) * (min(we, in.W) - max(ws, 0));
-          const float inv = 1.0f / (float)div;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] *= inv;
-        }
-        break;
-      }
-      case PK_DWCONV: {
-        // ReLU(sum_i w_i x_i) -> depthwise k x k; weights fp32 [C][kh*kw]
-        const float* wd = reinterpret_cast<const float*>(P.wts);
-        const float* aw = reinterpret_cast<const float*>(P.add_w);
-        const View& in0 = views[P.in_begin];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-        const int hs = oh * P.sh - P.ph, ws = ow * P.sw - P.pw;
-        const int kk = P.kh * P.kw;
-        for (int i = 0; i < P.kh; ++i) {
-          const int ih = hs + i;
-          if (ih < 0 || ih >= in0.H) continue;
-          for (int j = 0; j < P.kw; ++j) {
-            const int iw = ws + j;
-            if (iw < 0 || iw >= in0.W) continue;
-            const int64_t ipix = ((int64_t)n * in0.H + ih) * in0.W + iw;
-            float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int s = 0; s < P.n_in; ++s) {
-              float x[8];
-              load_vec(views[P.in_begin + s], dtype, ipix, c, x, nv);
-              const float w = aw ? aw[s] : 1.0f;
-#pragma unroll
-              for (int e = 0; e < 8; ++e) a[e] = fmaf(w, x[e], a[e]);
-            }
-            const int tap = i * P.kw + j;
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (e < nv) acc[e] = fmaf(wd[(c + e) * kk + tap], fmaxf(a[e], 0.f), acc[e]);
-          }
-        }
-        break;
-      }
-      case PK_COPY:
-      default: {
-        // concat gather (element-wise: inputs may have channel counts that are not vector multiples)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          acc[e] = 0.f;
-          if (e >= nv) continue;
-          int ch = c + e, off = 0;
-          for (int i = 0; i < P.n_in; ++i) {
-            const View& vi = views[P.in_begin + i];
-            const int ci = vi.Cl;
-            if (ch < off + ci) {
-              acc[e] = load_elem(vi, dtype, pix, ch - off);
-              break;
-            }
-            off += ci;
-          }
-        }
-        break;
       }
     }
-    store_vec(out, dtype, pix, c, acc);
+    store_vec(out, DT, pix, c, acc);
   }
 }
-
 
 // --------------------------------------------------------------------------------- the kernel
 struct Ring {          // smem ring iterator (slot, phase)
@@ -371,17 +391,55 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   uint64_t* tempty = bars + 2 * kStages + 2;                // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+  float* sbias_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // 2 x kMaxBN
+  uint8_t* sdesc = reinterpret_cast<uint8_t*>(bars) + kBarBytes + kBiasBytes;           // kDescBytes
   __shared__ int sm_tile_begin[kMaxProblems];
 
-  const Problem* probs = reinterpret_cast<const Problem*>(sd.problems);
-  const View* views = reinterpret_cast<const View*>(sd.views);
-  const Segment* segs = reinterpret_cast<const Segment*>(sd.segs);
+  // The descriptor table is copied into shared memory once, so every role decodes its tiles from
+  // smem instead of a chain of dependent global loads.
+  const bool desc_in_smem = sd.blob_bytes <= kDescBytes;
+  const uint8_t* dbase = desc_in_smem ? sdesc : reinterpret_cast<const uint8_t*>(sd.problems);
+  const Problem* probs = reinterpret_cast<const Problem*>(dbase);
+  const View* views = reinterpret_cast<const View*>(dbase + sd.views_off);
+  const Segment* segs = reinterpret_cast<const Segment*>(dbase + sd.segs_off);
   int* counters = reinterpret_cast<int*>(sd.counters);
   int* err = reinterpret_cast<int*>(sd.err);
+  // optional per-CTA timeline (ns, %globaltimer) for tools/trace_stage.py; slots: 0 entry, 1 prologue
+  // done, 2 first GEMM tile A issued, 3 producer done, 4 MMA done, 5 first accumulator ready,
+  // 6 epilogue/SIMT done, 7 teardown, 8 exit
+  uint64_t* trace = sd.trace ? reinterpret_cast<uint64_t*>(sd.trace) + blockIdx.x * 16 : nullptr;
+  bool tfirst = trace != nullptr;   // register flag: stamp only the first tile of each role
+#define IOS_TRACE(slot)                   \
+  do {                                    \
+    if (trace) trace[(slot)] = gtimer();  \
+  } while (0)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) IOS_TRACE(0);
+#ifdef IOS_LATPROBE
+  if (tid == 0 && trace) {
+    const int* q = reinterpret_cast<const int*>(sd.problems);
+    uint64_t a = gtimer();
+    int v1 = __ldcg(q + 64 * (blockIdx.x % 8));
+    uint64_t b = gtimer();
+    int v2 = __ldcg(q + 64 * (blockIdx.x % 8) + 32 * (v1 & 1) + 16);
+    uint64_t c = gtimer();
+    trace[13] = b - a + (v2 == 12345 ? 1 : 0);
+    trace[14] = c - b;
+    long long k0 = clock64();
+    uint64_t d0 = gtimer();
+    while (clock64() - k0 < 10000) {}
+    trace[15] = gtimer() - d0;   // ns for 10000 SM cycles -> SM clock
+  }
+#endif
 
-  for (int i = tid; i < sd.n_problems; i += kThreads) sm_tile_begin[i] = probs[i].tile_begin;
+  if (desc_in_smem) {
+    const int4* src = reinterpret_cast<const int4*>(sd.problems);
+    int4* dst = reinterpret_cast<int4*>(sdesc);
+    for (int i = tid; i < (sd.blob_bytes + 15) / 16; i += kThreads) dst[i] = __ldg(src + i);
+  }
+  for (int i = tid; i < sd.n_problems; i += kThreads)
+    sm_tile_begin[i] = reinterpret_cast<const Problem*>(sd.problems)[i].tile_begin;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(smem_u32(&full[s]), kProducerWarps * 32 + 1);
@@ -404,86 +462,113 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (tid == 0) IOS_TRACE(1);
 
-  if (warp < kProducerWarps) {
+  if (!sd.has_gemm) {
+    // ============================================================== SIMT-only stage: all warps
+    int hint = 0;
+    for (int t = blockIdx.x; t < sd.n_tiles; t += gridDim.x) {
+      hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
+      const Problem& P = probs[hint];
+      if (tid == 0) wait_deps(P, counters, err);
+      named_bar(3, kThreads);
+#ifndef IOS_NO_SIMT
+      simt_tile<DT>(P, views, t - P.tile_begin, tid, kThreads);
+#endif
+      named_bar(3, kThreads);
+      if (tid == 0 && P.signal) {
+        __threadfence();
+        atomicAdd(counters + P.done_idx, 1);
+      }
+    }
+  } else if (warp < kProducerWarps) {
     // ============================================================== PRODUCER (A gather + B bulk)
+    // Lean per-tile setup (fast divisions; per-row pixel offsets once per tile) and an incremental
+    // im2col walk: each thread owns 2 pieces (16 B) x 4 rows of every 128 B K-chunk; a piece's
+    // (tap row, tap col, channel) advance by one chunk per iteration without any division.
     const int ptid = tid;                       // 0..127
     const int rig = lane & 7;                   // row inside an 8-row core-matrix group
     const int pc0 = lane >> 3;                  // pieces pc0 and pc0 + 4 of each 128 B chunk row
+    constexpr int ESZ = DT == ET_BF16 ? 2 : 4;
+    constexpr int VEC = 16 / ESZ, ELEMS = kChunkBytes / ESZ;
     Ring ring;
     int hint = 0;
     for (int t = blockIdx.x; t < sd.n_tiles; t += gridDim.x) {
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
       if (P.kind != PK_GEMM) continue;
-      if (ptid == 0) wait_deps(P, counters, err);
-      named_bar(1, 128);
+      if (P.n_deps) {
+        if (ptid == 0) wait_deps(P, counters, err);
+        named_bar(1, 128);
+      }
       const int local = t - P.tile_begin;
-      const int s = local % P.split;
-      const int rest = local / P.split;
-      const int nt = rest % P.n_tiles_n;
-      const int mt = rest / P.n_tiles_n;
+      const int rest = fdiv(P.fd_split, local);
+      const int s = local - rest * P.split;
+      const int mt = fdiv(P.fd_ntn, rest);
+      const int nt = rest - mt * P.n_tiles_n;
       const int c0 = s * P.chunks_per_split;
       const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
+      // everything the chunk loop needs lives in registers: the cp.async asm statements clobber
+      // "memory", which would otherwise force the descriptor fields to be re-read from smem
       const View in = views[P.in_begin];
-      const int esz = P.dtype == ET_BF16 ? 2 : 4;
-      const int vec = 16 / esz;
-      const int elems = kChunkBytes / esz;
-      const int HoWo = P.Ho * P.Wo;
+      const int inC = in.C, inH = in.H, inW = in.W, cstride = in.cstride;
+      const int kh = P.kh, kw = P.kw;
       const bool relu_pre = (P.flags & 2) != 0;
-      // per-row state for the 4 rows this thread gathers
-      int ih0[4], iw0[4];
-      int64_t rbase[4];
-      bool rvalid[4];
+      int roff[4], ih0[4], iw0[4];   // row pixel offset (may be negative: padding) and window origin
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int r = (warp + 4 * j) * 8 + rig;
-        const int m = mt * kBM + r;
-        rvalid[j] = m < P.M;
-        const int mm = rvalid[j] ? m : 0;
-        const int n = mm / HoWo;
-        const int rem = mm - n * HoWo;
-        const int oh = rem / P.Wo, ow = rem - (rem / P.Wo) * P.Wo;
+        const int m = mt * kBM + (warp + 4 * j) * 8 + rig;
+        const int n = fdiv(P.fd_howo, m);
+        const int rem = m - n * (P.Ho * P.Wo);
+        const int oh = fdiv(P.fd_wo, rem);
+        const int ow = rem - oh * P.Wo;
         ih0[j] = oh * P.sh - P.ph;
         iw0[j] = ow * P.sw - P.pw;
-        rbase[j] = (int64_t)n * in.H * in.W;
+        roff[j] = m < P.M ? (n * inH + ih0[j]) * inW + iw0[j] : INT_MIN;   // INT_MIN: row past M
       }
-      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts);
+      // piece state at chunk c0: k = c0*ELEMS + pc*VEC = tap*C + ci, tap = ti*kw + tj
+      int ti[2], tj[2], ci[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = c0 * ELEMS + (pc0 + 4 * h) * VEC;
+        const int tap = fdiv(P.fd_cin, k);
+        ci[h] = k - tap * inC;
+        ti[h] = fdiv(P.fd_kw, tap);
+        tj[h] = tap - ti[h] * kw;
+      }
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)nt * (P.BN >> 3) * 1024;
+      const int64_t wstep = (int64_t)(P.Npad8 >> 3) * 1024;
       // the last n tile may run past the packed rows: copy only those (the rest of the smem tile is
       // stale and only feeds accumulator columns that no output segment covers)
       const uint32_t bbytes = (uint32_t)min(P.BN, P.Npad8 - nt * P.BN) * kChunkBytes;
+      const char* ibase = reinterpret_cast<const char*>(in.ptr) + (int64_t)in.coff * ESZ;
       int pend[2] = {-1, -1};
       for (int c = c0; c < c1; ++c) {
         mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
         if (ptid == 0) {
           const uint32_t fb = smem_u32(&full[ring.slot]);
           mbar_arrive_expect_tx(fb, bbytes);
-          const uint8_t* src = wsrc + ((int64_t)c * (P.Npad8 >> 3) + (int64_t)nt * (P.BN >> 3)) * 1024;
-          bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), src, bbytes, fb);
+          bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
         }
-        uint8_t* a_st = sA + ring.slot * kAStageBytes;
+        const uint32_t a_st = smem_u32(sA + ring.slot * kAStageBytes) + rig * 16 + pc0 * 128;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int pc = pc0 + 4 * h;
-          const int k = c * elems + pc * vec;
-          const bool kvalid = k < P.K;
-          const int tap = k / in.C;
-          const int ci = k - tap * in.C;
-          const int ki = tap / P.kw, kj = tap - (tap / P.kw) * P.kw;
+          const bool kvalid = ti[h] < kh;                            // k < K
+          const int toff = (ti[h] * inW + tj[h]) * cstride + ci[h];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const int r = (warp + 4 * j) * 8 + rig;
-            const int ih = ih0[j] + ki, iw = iw0[j] + kj;
-            const bool ok = kvalid && rvalid[j] && ih >= 0 && ih < in.H && iw >= 0 && iw < in.W;
-            const int64_t eoff = ok ? ((rbase[j] + (int64_t)ih * in.W + iw) * in.cstride + in.coff + ci) : 0;
-            const uint8_t* src = reinterpret_cast<const uint8_t*>(in.ptr) + eoff * esz;
-            uint8_t* dst = a_st + (r >> 3) * 1024 + pc * 128 + (r & 7) * 16;
+            if (roff[j] == INT_MIN) continue;                        // row past M: never stored
+            const int ih = ih0[j] + ti[h], iw = iw0[j] + tj[h];
+            const bool ok = kvalid && (unsigned)ih < (unsigned)inH && (unsigned)iw < (unsigned)inW;
+            // padding taps / K tail: zero fill without reading (ignore-src)
+            const char* src = ibase + ((int64_t)roff[j] * cstride + (ok ? toff : 0)) * ESZ;
+            const uint32_t dst = a_st + (warp + 4 * j) * 1024 + h * 512;
             if (!relu_pre) {
-              cp_async16(smem_u32(dst), src, ok ? 16u : 0u);
+              cp_async16_zfill(dst, ok ? src : ibase, !ok);
             } else {
               uint4 v = make_uint4(0, 0, 0, 0);
               if (ok) v = __ldcg(reinterpret_cast<const uint4*>(src));
-              if (esz == 4) {
+              if (ESZ == 4) {
                 float* f = reinterpret_cast<float*>(&v);
                 f[0] = fmaxf(f[0], 0.f); f[1] = fmaxf(f[1], 0.f); f[2] = fmaxf(f[2], 0.f); f[3] = fmaxf(f[3], 0.f);
               } else {
@@ -491,11 +576,22 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
                 const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
                 hb[0] = __hmax2(hb[0], z); hb[1] = __hmax2(hb[1], z); hb[2] = __hmax2(hb[2], z); hb[3] = __hmax2(hb[3], z);
               }
-              *reinterpret_cast<uint4*>(dst) = v;
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(v.x), "r"(v.y), "r"(v.z),
+                           "r"(v.w) : "memory");
+            }
+          }
+          // advance this piece by one chunk (ELEMS elements of K)
+          ci[h] += ELEMS;
+          while (ci[h] >= inC) {
+            ci[h] -= inC;
+            if (++tj[h] == kw) {
+              tj[h] = 0;
+              ++ti[h];
             }
           }
         }
         cp_async_commit();
+        if (ptid == 0 && tfirst && c - c0 < 3) IOS_TRACE(c == c0 ? 2 : 8 + c - c0);
         // arrive for the chunk issued two iterations ago (keeps up to 3 chunks of cp.async in flight)
         if (pend[0] >= 0) {
           cp_async_wait<2>();
@@ -507,6 +603,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         ring.next();
       }
       cp_async_wait<0>();
+      if (ptid == 0 && tfirst) IOS_TRACE(12);
+      tfirst = false;
       fence_proxy_async();
       if (pend[0] >= 0) mbar_arrive(smem_u32(&full[pend[0]]));
       if (pend[1] >= 0) mbar_arrive(smem_u32(&full[pend[1]]));
@@ -525,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const Problem& P = probs[hint];
         if (P.kind != PK_GEMM) continue;
         const int local = t - P.tile_begin;
-        const int s = local % P.split;
+        const int s = local - fdiv(P.fd_split, local) * P.split;
         const int c0 = s * P.chunks_per_split;
         const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
         const uint32_t idesc = umma_idesc(DT == ET_BF16, P.BN);
@@ -567,28 +665,79 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       if (P.kind != PK_GEMM) {
         if (etid == 0) wait_deps(P, counters, err);
         named_bar(2, 128);
-        simt_tile(P, views, t - P.tile_begin, etid);
+#ifndef IOS_NO_SIMT
+        simt_tile<DT>(P, views, t - P.tile_begin, etid, 128);
+#endif
         named_bar(2, 128);
-        if (etid == 0) {
+        if (etid == 0 && P.signal) {
           __threadfence();
           atomicAdd(counters + P.done_idx, 1);
         }
         continue;
       }
       const int local = t - P.tile_begin;
-      const int s = local % P.split;
-      const int rest = local / P.split;
-      const int nt = rest % P.n_tiles_n;
-      const int mt = rest / P.n_tiles_n;
+      const int rest = fdiv(P.fd_split, local);
+      const int s = local - rest * P.split;
+      const int mt = fdiv(P.fd_ntn, rest);
+      const int nt = rest - mt * P.n_tiles_n;
       const int m = mt * kBM + etid;
       const bool valid = m < P.M;
       const int esz_out = P.dtype == ET_BF16 ? 2 : 4;
       const float* bias = reinterpret_cast<const float*>(P.bias);
+      // stage this tile's bias slice in smem while the MMAs run (one load round trip, off the
+      // critical path); the previous tile's readers of this buffer are past the barrier below
+      float* sbias = sbias_all + acc * kMaxBN;
+      for (int i = etid; i < P.BN; i += 128) sbias[i] = __ldg(bias + nt * P.BN + i);
+      named_bar(2, 128);
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+      if (etid == 0 && tfirst) IOS_TRACE(5);
+      tfirst = false;
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
       const int out_tile = mt * P.n_tiles_n + nt;
-      if (P.split == 1) {
+      if (P.split == 1 && P.n_seg == 1) {
+        // one output segment (every non-merged GEMM): row address once, 32 columns per TMEM round
+        constexpr int OESZ = DT == ET_BF16 ? 2 : 4;
+        const Segment& sg = segs[P.seg_begin];
+        const int nend = sg.n1, relu = sg.relu;
+        char* orow = reinterpret_cast<char*>(sg.out.ptr) +
+                     ((int64_t)m * sg.out.cstride + sg.out.coff - sg.n0) * OESZ;
+        for (int c0 = 0; c0 < P.BN; c0 += 32) {
+          uint32_t va[16], vb[16];
+          tmem_ld16(tbase + c0, va);
+          tmem_ld16(tbase + c0 + 16, vb);
+          tmem_ld_wait();
+          if (!valid) continue;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int ncol = nt * P.BN + c0 + g * 8;
+            if (c0 + g * 8 >= P.BN || ncol >= nend) break;
+            const float4 b0 = *reinterpret_cast<const float4*>(sbias + c0 + g * 8);
+            const float4 b1 = *reinterpret_cast<const float4*>(sbias + c0 + g * 8 + 4);
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            float o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const uint32_t raw = g < 2 ? va[g * 8 + e] : vb[(g - 2) * 8 + e];
+              o[e] = __uint_as_float(raw) + bb[e];
+              if (relu) o[e] = fmaxf(o[e], 0.f);
+            }
+            if (DT == ET_BF16) {
+              uint4 pk;
+              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+              *reinterpret_cast<uint4*>(orow + (int64_t)ncol * OESZ) = pk;
+            } else {
+              float4* dst = reinterpret_cast<float4*>(orow + (int64_t)ncol * OESZ);
+              dst[0] = make_float4(tf32_round(o[0]), tf32_round(o[1]), tf32_round(o[2]), tf32_round(o[3]));
+              dst[1] = make_float4(tf32_round(o[4]), tf32_round(o[5]), tf32_round(o[6]), tf32_round(o[7]));
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty[acc]));
+      } else if (P.split == 1) {
         for (int c0 = 0; c0 < P.BN; c0 += 16) {
           uint32_t v[16];
           tmem_ld16(tbase + c0, v);
@@ -626,11 +775,13 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           uint32_t v[16];
           tmem_ld16(tbase + c0, v);
           tmem_ld_wait();
+          if (valid) {
 #pragma unroll
-          for (int q = 0; q < 16; q += 4)
-            __stcg(reinterpret_cast<float4*>(mine + c0 + q),
-                   make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]), __uint_as_float(v[q + 2]),
-                               __uint_as_float(v[q + 3])));
+            for (int q = 0; q < 16; q += 4)
+              __stcg(reinterpret_cast<float4*>(mine + c0 + q),
+                     make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]), __uint_as_float(v[q + 2]),
+                                 __uint_as_float(v[q + 3])));
+          }
         }
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty[acc]));
@@ -642,39 +793,49 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         }
         named_bar(2, 128);
         const bool last = *flag != 0;
-        if (last) {
+        if (last && valid) {
           __threadfence();
-          if (valid) {
-            for (int c0 = 0; c0 < P.BN; c0 += 8) {
-              const int ncol = nt * P.BN + c0;
-              const Segment* sgp = nullptr;
-              for (int q = 0; q < P.n_seg; ++q) {
-                const Segment& sg = segs[P.seg_begin + q];
-                if (ncol >= sg.n0 && ncol < sg.n1) {
-                  sgp = &sg;
-                  break;
-                }
+          // deterministic: partials summed in split order 0..split-1, 8 splits' loads in flight
+          const int64_t sstride = (int64_t)kBM * P.BN;
+          const float* base = ws + ((int64_t)out_tile * P.split * kBM + etid) * P.BN;
+          for (int c0 = 0; c0 < P.BN; c0 += 8) {
+            const int ncol = nt * P.BN + c0;
+            const Segment* sgp = nullptr;
+            for (int q = 0; q < P.n_seg; ++q) {
+              const Segment& sg = segs[P.seg_begin + q];
+              if (ncol >= sg.n0 && ncol < sg.n1) {
+                sgp = &sg;
+                break;
               }
-              if (!sgp) continue;
-              float o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-              for (int ss = 0; ss < P.split; ++ss) {
-                const float* src = ws + (((int64_t)out_tile * P.split + ss) * kBM + etid) * P.BN + c0;
-                const float4 x0 = __ldcg(reinterpret_cast<const float4*>(src));
-                const float4 x1 = __ldcg(reinterpret_cast<const float4*>(src + 4));
-                o[0] += x0.x; o[1] += x0.y; o[2] += x0.z; o[3] += x0.w;
-                o[4] += x1.x; o[5] += x1.y; o[6] += x1.z; o[7] += x1.w;
-              }
-              const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + ncol));
-              const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + ncol + 4));
-              const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                o[e] += bb[e];
-                if (sgp->relu) o[e] = fmaxf(o[e], 0.f);
-              }
-              store_vec(sgp->out, P.dtype, m, ncol - sgp->n0, o);
-              if (esz_out == 4) store_vec(sgp->out, P.dtype, m, ncol - sgp->n0 + 4, o + 4);
             }
+            if (!sgp) continue;
+            float o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int s0 = 0; s0 < P.split; s0 += 8) {
+              float4 x[8][2];
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (s0 + u < P.split) {
+                  const float* src = base + (s0 + u) * sstride + c0;
+                  x[u][0] = __ldcg(reinterpret_cast<const float4*>(src));
+                  x[u][1] = __ldcg(reinterpret_cast<const float4*>(src + 4));
+                }
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (s0 + u < P.split) {
+                  o[0] += x[u][0].x; o[1] += x[u][0].y; o[2] += x[u][0].z; o[3] += x[u][0].w;
+                  o[4] += x[u][1].x; o[5] += x[u][1].y; o[6] += x[u][1].z; o[7] += x[u][1].w;
+                }
+            }
+            const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + ncol));
+            const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + ncol + 4));
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              o[e] += bb[e];
+              if (sgp->relu) o[e] = fmaxf(o[e], 0.f);
+            }
+            store_vec(sgp->out, DT, m, ncol - sgp->n0, o);
+            if (DT != ET_BF16) store_vec(sgp->out, DT, m, ncol - sgp->n0 + 4, o + 4);
           }
         }
         if (!last) {
@@ -683,16 +844,20 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           continue;
         }
       }
-      named_bar(2, 128);
-      if (etid == 0) {
-        __threadfence();
-        atomicAdd(counters + P.done_idx, 1);
+      if (P.signal) {
+        named_bar(2, 128);
+        if (etid == 0) {
+          __threadfence();
+          atomicAdd(counters + P.done_idx, 1);
+        }
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1u;
     }
   }
 
+  if (trace && (tid == 0 || tid == kEpilogueWarp0 * 32 || tid == kMmaWarp * 32))
+    IOS_TRACE(tid == 0 ? 3 : tid == kMmaWarp * 32 ? 4 : 6);
   // ---------------------------------------------------------------------------- teardown
   __syncwarp();   // the MMA warp ran its loop on lane 0 only
   tc_fence_before();
@@ -704,6 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   if (tid == 0) {
     // the last CTA out resets the stage's counters for the next launch (graph-replay safe)
     __threadfence();
+    IOS_TRACE(7);
     const int old = atomicAdd(counters, 1);
     if (old == (int)gridDim.x - 1) {
       __threadfence();
@@ -711,7 +877,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       __threadfence();
       counters[0] = 0;
     }
+    IOS_TRACE(8);
   }
+#undef IOS_TRACE
 }
 
 // ------------------------------------------------------------------------ boundary layout kernels

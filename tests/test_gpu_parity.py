@@ -87,3 +87,20 @@ def test_ios_stage_latency_positive(torch_cuda):
     t_all = g.stage_latency([1, 2, 3, 4])
     t_m = g.stage_latency([1, 3, 4], MERGE)
     assert 0 < t1 < 1.0 and 0 < t_all < 1.0 and 0 < t_m < 1.0
+
+
+@pytest.mark.parametrize("name,math", [("inception_v3", "tf32"), ("squeezenet", "tf32"), ("randwire_ws_small", "bf16"),
+                                       ("nasnet_a_large", "tf32")])
+def test_network_sequential_and_greedy(torch_cuda, name, math):
+    """Full networks at BASELINE.json's sizes: per-op parity (every op, oracle fed the GPU's inputs)
+    under the sequential schedule, end-to-end parity under sequential and greedy."""
+    net = W.build(name, math=math)
+    x = net.make_input()
+    ref = OracleGraph(net).run_sequential(x)[net.n_ops]
+    g, q, y = _run(net, math, "sequential", torch_cuda)
+    errs = per_op_errors(net, g, math)
+    worst = max(errs, key=errs.get)
+    assert errs[worst] < TOL[math], (worst, net.op(worst).name, errs[worst])
+    assert rel_err(y, ref) < TOL[math]
+    _, _, y2 = _run(net, math, "greedy", torch_cuda)
+    assert rel_err(y2, ref) < TOL[math]

@@ -1,0 +1,26 @@
+"""Per-CTA timeline of one stage launch (ios_stage_trace), relative to the earliest CTA entry."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import workloads as W
+from paper_2011_01302_b200 import Graph
+from paper_2011_01302_b200.ios import lib, _check, _i32
+net = W.build(sys.argv[1])
+g = Graph.from_netspec(net)
+stages = eval(sys.argv[2])
+lib.ios_stage_trace.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.POINTER(C.c_uint64), C.c_int32, C.POINTER(C.c_int32)]
+for ops, t in stages:
+    ms = g.stage_latency(ops, t)
+    buf = (C.c_uint64 * (148 * 16))()
+    grid = C.c_int32()
+    _check(lib.ios_stage_trace(g.handle, _i32(ops), len(ops), t, buf, 148 * 16, C.byref(grid)))
+    a = np.array(buf[:grid.value * 16], dtype=np.int64).reshape(grid.value, 16)[:, :13]
+    t0 = a[:, 0][a[:, 0] > 0].min()
+    rel = np.where(a > 0, (a - t0) / 1000.0, np.nan)
+    print(f"stage {ops} T={t} profiled {ms*1e3:.1f} us, grid {grid.value}; us since first entry (min/median/max over CTAs):")
+    names = ["entry", "prologue", "A1 issued", "prod done", "mma done", "acc1 ready", "epi done", "teardown", "exit", "A2 issued", "A3 issued", "-", "A landed"]
+    for k, nm in enumerate(names):
+        col = rel[:, k]
+        col = col[~np.isnan(col)]
+        if len(col):
+            print(f"   {nm:11s} {col.min():8.2f} {np.median(col):8.2f} {col.max():8.2f}  (n={len(col)})")
