@@ -516,7 +516,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       p.n_tiles = s.mt * s.ntn * s.split;
       if (p.split > 1) {
         p.workspace = ws_bytes;   // offset for now
-        ws_bytes += (size_t)s.mt * s.ntn * s.split * kBM * s.BN * sizeof(float);
+        ws_bytes += (size_t)s.mt * s.ntn * kBM * s.BN * sizeof(float);   // zeroed fp32 accumulators (red.add)
         p.tilectr_idx = n_tilectr;
         n_tilectr += s.mt * s.ntn;
       }

@@ -768,9 +768,11 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty[acc]));
       } else {
-        // split-K: write the fp32 partial, the last arriving split reduces in split order
+        // split-K: every split adds its fp32 partial into the tile's zeroed accumulator with
+        // vector reductions (fire-and-forget at L2); the last arriving split reads the sum once,
+        // applies bias/ReLU, stores, and re-zeroes the accumulator for the next launch.
         float* ws = reinterpret_cast<float*>(P.workspace);
-        float* mine = ws + (((int64_t)out_tile * P.split + s) * kBM + etid) * P.BN;
+        float* mine = ws + ((int64_t)out_tile * kBM + etid) * P.BN;
         for (int c0 = 0; c0 < P.BN; c0 += 16) {
           uint32_t v[16];
           tmem_ld16(tbase + c0, v);
@@ -778,9 +780,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           if (valid) {
 #pragma unroll
             for (int q = 0; q < 16; q += 4)
-              __stcg(reinterpret_cast<float4*>(mine + c0 + q),
-                     make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]), __uint_as_float(v[q + 2]),
-                                 __uint_as_float(v[q + 3])));
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mine + c0 + q), "r"(v[q]),
+                           "r"(v[q + 1]), "r"(v[q + 2]), "r"(v[q + 3])
+                           : "memory");
           }
         }
         tc_fence_before();
@@ -795,9 +797,6 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const bool last = *flag != 0;
         if (last && valid) {
           __threadfence();
-          // deterministic: partials summed in split order 0..split-1, 8 splits' loads in flight
-          const int64_t sstride = (int64_t)kBM * P.BN;
-          const float* base = ws + ((int64_t)out_tile * P.split * kBM + etid) * P.BN;
           for (int c0 = 0; c0 < P.BN; c0 += 8) {
             const int ncol = nt * P.BN + c0;
             const Segment* sgp = nullptr;
@@ -808,26 +807,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
                 break;
               }
             }
+            float4* src = reinterpret_cast<float4*>(mine + c0);
+            const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+            __stcg(src, make_float4(0.f, 0.f, 0.f, 0.f));
+            __stcg(src + 1, make_float4(0.f, 0.f, 0.f, 0.f));
             if (!sgp) continue;
-            float o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int s0 = 0; s0 < P.split; s0 += 8) {
-              float4 x[8][2];
-#pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (s0 + u < P.split) {
-                  const float* src = base + (s0 + u) * sstride + c0;
-                  x[u][0] = __ldcg(reinterpret_cast<const float4*>(src));
-                  x[u][1] = __ldcg(reinterpret_cast<const float4*>(src + 4));
-                }
-#pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (s0 + u < P.split) {
-                  o[0] += x[u][0].x; o[1] += x[u][0].y; o[2] += x[u][0].z; o[3] += x[u][0].w;
-                  o[4] += x[u][1].x; o[5] += x[u][1].y; o[6] += x[u][1].z; o[7] += x[u][1].w;
-                }
-            }
-            const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + ncol));
-            const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + ncol + 4));
+            float o[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            const float4 b0 = *reinterpret_cast<const float4*>(sbias + c0);
+            const float4 b1 = *reinterpret_cast<const float4*>(sbias + c0 + 4);
             const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
