@@ -147,7 +147,11 @@ def run_ours(args):
 
     g = Graph.from_netspec(net, spec["math"], local)
     t0 = time.time()
+    if args.latency_cache and os.path.exists(args.latency_cache):
+        g.load_latency_cache(args.latency_cache)              # resume: measured stage latencies
     q_ios = g.schedule_dp(args.r, args.s)                      # device-measured stage costs (Alg. 1)
+    if args.latency_cache and not os.path.exists(args.latency_cache):
+        g.save_latency_cache(args.latency_cache)
     search_s = time.time() - t0
     q_seq = g.schedule_sequential()
     q_greedy = g.schedule_greedy()
@@ -338,6 +342,7 @@ def main():
     ap.add_argument("--r", type=int, default=3)
     ap.add_argument("--s", type=int, default=8)
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
+    ap.add_argument("--latency-cache", default="", help="load (if present) / save the DP's stage-latency cache")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
