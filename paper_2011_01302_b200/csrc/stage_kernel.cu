@@ -84,6 +84,19 @@ __device__ __forceinline__ uint64_t gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// completion signal: release-ordered add (orders this CTA's prior writes, observed through the
+// preceding bar.sync, before the counter update) — no full membar / L1 invalidate
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_acqrel_add(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+// programmatic dependent launch: let the next stage's grid launch now; wait for the previous one
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -462,6 +475,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch: the prologue above overlapped the previous stage's tail; from
+  // here on we read activations (and counters) the previous grid may still be writing
+  pdl_wait();
+  pdl_launch_dependents();
   if (tid == 0) IOS_TRACE(1);
 
   if (!sd.has_gemm) {
@@ -476,10 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       simt_tile<DT>(P, views, t - P.tile_begin, tid, kThreads);
 #endif
       named_bar(3, kThreads);
-      if (tid == 0 && P.signal) {
-        __threadfence();
-        atomicAdd(counters + P.done_idx, 1);
-      }
+      if (tid == 0 && P.signal) red_release_add(counters + P.done_idx, 1);
     }
   } else if (warp < kProducerWarps) {
     // ============================================================== PRODUCER (A gather + B bulk)
@@ -669,10 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         simt_tile<DT>(P, views, t - P.tile_begin, etid, 128);
 #endif
         named_bar(2, 128);
-        if (etid == 0 && P.signal) {
-          __threadfence();
-          atomicAdd(counters + P.done_idx, 1);
-        }
+        if (etid == 0 && P.signal) red_release_add(counters + P.done_idx, 1);
         continue;
       }
       const int local = t - P.tile_begin;
@@ -787,16 +798,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         }
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty[acc]));
-        __threadfence();
         named_bar(2, 128);
         if (etid == 0) {
-          const int old = atomicAdd(counters + P.tilectr_idx + out_tile, 1);
+          const int old = atom_acqrel_add(counters + P.tilectr_idx + out_tile, 1);
           *flag = (old == P.split - 1);
         }
         named_bar(2, 128);
         const bool last = *flag != 0;
         if (last && valid) {
-          __threadfence();
           for (int c0 = 0; c0 < P.BN; c0 += 8) {
             const int ncol = nt * P.BN + c0;
             const Segment* sgp = nullptr;
@@ -833,10 +842,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       }
       if (P.signal) {
         named_bar(2, 128);
-        if (etid == 0) {
-          __threadfence();
-          atomicAdd(counters + P.done_idx, 1);
-        }
+        if (etid == 0) red_release_add(counters + P.done_idx, 1);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1u;
@@ -854,15 +860,15 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols) : "memory");
   }
   if (tid == 0) {
-    // the last CTA out resets the stage's counters for the next launch (graph-replay safe)
-    __threadfence();
     IOS_TRACE(7);
-    const int old = atomicAdd(counters, 1);
-    if (old == (int)gridDim.x - 1) {
-      __threadfence();
-      for (int i = 1; i < sd.n_counters; ++i) counters[i] = 0;
-      __threadfence();
-      counters[0] = 0;
+    if (sd.n_counters > 1) {
+      // the last CTA out resets the stage's counters for the next launch (graph-replay safe)
+      const int old = atom_acqrel_add(counters, 1);
+      if (old == (int)gridDim.x - 1) {
+        for (int i = 1; i < sd.n_counters; ++i) counters[i] = 0;
+        __threadfence();
+        counters[0] = 0;
+      }
     }
     IOS_TRACE(8);
   }
@@ -911,11 +917,18 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  if (dtype == ET_BF16)
-    ios_stage_kernel<ET_BF16><<<grid, kThreads, kSmemBytes + 1024, st>>>(sd);
-  else
-    ios_stage_kernel<ET_F32><<<grid, kThreads, kSmemBytes + 1024, st>>>(sd);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes + 1024;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (dtype == ET_BF16) return cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_BF16>, sd);
+  return cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32>, sd);
 }
 
 cudaError_t launch_nchw_to_nhwc(const float* in, const View& out, int dtype, int N, int C, cudaStream_t st) {
