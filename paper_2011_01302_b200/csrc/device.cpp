@@ -10,6 +10,8 @@
 #include <cstring>
 #include <limits>
 
+#include <cuda.h>
+
 #include "ios_core.h"
 
 namespace ios {
@@ -508,6 +510,9 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       p.fd_ntn = make_fastdiv((uint32_t)s.ntn);
       p.fd_cin = make_fastdiv((uint32_t)in.C);
       p.fd_kw = make_fastdiv((uint32_t)p.kw);
+      // A via TMA when it is a plain [M, C] matrix: 1x1, stride 1, no padding, no pre-ReLU
+      p.a_tma = (p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 && p.pw == 0 &&
+                 !(p.flags & IOS_F_RELU_PRE)) ? 1 : 0;
       p.BN = s.BN;
       p.n_tiles_n = s.ntn;
       p.m_tiles = s.mt;
@@ -554,6 +559,36 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       std::memcpy(blob.data(), b.probs.data(), pb);
       if (vb) std::memcpy(blob.data() + pb, b.views.data(), vb);
       if (sb) std::memcpy(blob.data() + pb + vb, b.segs.data(), sb);
+      // tensor maps for TMA-loaded A operands (global memory, 64 B aligned, written before launch)
+      std::vector<CUtensorMap> maps;
+      for (Problem& p : b.probs) {
+        if (p.kind != PK_GEMM || !p.a_tma) continue;
+        const View& in = b.views[p.in_begin];
+        CUtensorMap tm;
+        const cuuint64_t dims[2] = {(cuuint64_t)in.C, (cuuint64_t)p.M};
+        const cuuint64_t strides[1] = {(cuuint64_t)in.cstride * g.esize()};
+        const cuuint32_t box[2] = {(cuuint32_t)(kChunkBytes / g.esize()), (cuuint32_t)kBM};
+        const cuuint32_t estr[2] = {1, 1};
+        void* base = reinterpret_cast<char*>(in.ptr) + (size_t)in.coff * g.esize();
+        CUresult r = cuTensorMapEncodeTiled(&tm, g.math == IOS_MATH_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                            2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+          p.a_tma = 0;   // fall back to the cp.async gather
+          continue;
+        }
+        p.tmap_a = maps.size();
+        maps.push_back(tm);
+      }
+      if (!maps.empty()) {
+        void* mp = dmalloc(d, maps.size() * sizeof(CUtensorMap));
+        IOS_CHECK_CUDA(cudaMemcpy(mp, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+        for (Problem& p : b.probs)
+          if (p.kind == PK_GEMM && p.a_tma) p.tmap_a = (uint64_t)mp + p.tmap_a * sizeof(CUtensorMap);
+      }
+      std::memcpy(blob.data(), b.probs.data(), pb);
       plan->dmem = upload(d, blob);
       plan->counters = static_cast<int*>(dmalloc(d, (size_t)n_counters * sizeof(int)));
       StageDesc& sd = plan->sd;
@@ -568,6 +603,8 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       sd.blob_bytes = (int)(pb + vb + sb);
       sd.views_off = (int)pb;
       sd.segs_off = (int)(pb + vb);
+      sd.uses_counters = 0;
+      for (Problem& p : b.probs) sd.uses_counters |= (p.signal || (p.kind == PK_GEMM && p.split > 1)) ? 1 : 0;
       sd.has_gemm = 0;
       for (Problem& p : b.probs) sd.has_gemm |= p.kind == PK_GEMM;
       plan->grid = std::min(tiles, d.num_sms);

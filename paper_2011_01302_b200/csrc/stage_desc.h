@@ -16,8 +16,9 @@ constexpr int kAStageBytes = kBM * kChunkBytes;         // 16 KB
 constexpr int kBStageBytes = kMaxBN * kChunkBytes;      // 32 KB
 constexpr int kBarBytes = 256;            // mbarriers, TMEM slot, flags
 constexpr int kBiasBytes = 2 * kMaxBN * 4; // bias slice per accumulator buffer
-constexpr int kDescBytes = 26 * 1024;     // stage descriptor table (problems | views | segments) copy
-constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + kBarBytes + kBiasBytes + kDescBytes;
+constexpr int kDescBytes = 14 * 1024;     // stage descriptor table (problems | views | segments) copy
+constexpr int kEpiBytes = 4 * 4096;       // epilogue staging: 32 rows x 128 B per epilogue warp
+constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + kBarBytes + kBiasBytes + kDescBytes + kEpiBytes;
 constexpr int kProducerWarps = 4;         // warps 0-3: A gather (cp.async) + B bulk copy
 constexpr int kEpilogueWarp0 = 4;         // warps 4-7: TMEM -> registers -> global; SIMT tiles
 constexpr int kMmaWarp = 8;               // warp 8: tcgen05.mma issuer + TMEM allocator
@@ -89,7 +90,8 @@ struct Problem {
   FastDiv fd_howo, fd_wo, fd_split, fd_ntn, fd_cin, fd_kw;   // divisors of the tile / im2col decode
   // SIMT geometry
   int32_t items_per_tile, n_items;  // items = output pixels (x channel vectors handled inside)
-  int32_t pad_[1];
+  int32_t a_tma;                    // 1: A is a plain [M, C] matrix (1x1 s1 conv) loaded by TMA
+  uint64_t tmap_a;                  // global address of its CUtensorMap (2D tiled, 128B swizzle)
 };
 
 struct StageDesc {
@@ -101,7 +103,8 @@ struct StageDesc {
   uint64_t trace;                   // optional uint64 [grid][16] timeline (0 = off)
   int32_t n_problems, n_tiles, n_counters, has_gemm;
   int32_t blob_bytes;               // problems | views | segments, contiguous from `problems`
-  int32_t views_off, segs_off, pad_;
+  int32_t views_off, segs_off;
+  int32_t uses_counters;            // any in-stage dependency or split-K: reset counters at exit
 };
 
 }  // namespace ios

@@ -54,6 +54,15 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(mbar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, uint64_t tmap, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cnt(uint32_t a, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
@@ -111,6 +120,17 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
+  return d;
+}
+// K-major SWIZZLE_128B (the TMA 128 B-swizzled tile): 8-row atoms of 1024 B (SBO), LBO unused (1);
+// the start address advances by 32 B per MMA K step inside the 128 B row.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
   return d;
 }
 // Instruction descriptor: D f32, A/B = tf32 (2) or bf16 (1), K-major both, N >> 3, M >> 4.
@@ -377,6 +397,9 @@ __device__ __noinline__ void simt_tile(const Problem& P, const View* views, int 
 struct Ring {          // smem ring iterator (slot, phase)
   int slot = 0;
   uint32_t phase = 0;
+  __device__ __forceinline__ void advance(int n) {
+    for (int i = 0; i < n; ++i) next();
+  }
   __device__ __forceinline__ void next() {
     if (++slot == kStages) {
       slot = 0;
@@ -406,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
   float* sbias_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // 2 x kMaxBN
   uint8_t* sdesc = reinterpret_cast<uint8_t*>(bars) + kBarBytes + kBiasBytes;           // kDescBytes
+  uint8_t* sepi = sdesc + kDescBytes;                                                     // kEpiBytes: 4 x 4 KB
   __shared__ int sm_tile_begin[kMaxProblems];
 
   // The descriptor table is copied into shared memory once, so every role decodes its tiles from
@@ -455,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     sm_tile_begin[i] = reinterpret_cast<const Problem*>(sd.problems)[i].tile_begin;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(smem_u32(&full[s]), kProducerWarps * 32 + 1);
+      mbar_init(smem_u32(&full[s]), kProducerWarps + 1);   // 4 producer warps + the expect_tx arrival
       mbar_init(smem_u32(&empty[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -522,6 +546,35 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const int nt = rest - mt * P.n_tiles_n;
       const int c0 = s * P.chunks_per_split;
       const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
+      if (P.a_tma) {
+        // A is a plain [M, C] matrix (1x1, stride 1): ONE tensor TMA per chunk (128 rows x 128 B,
+        // 128 B swizzle, rows past M / channels past C zero-filled) + one bulk copy for B, both
+        // issued by one thread; warps 1-3 only keep their ring position in step.
+        if (warp == 0) {
+          const uint64_t tmap = P.tmap_a;
+          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)nt * (P.BN >> 3) * 1024;
+          const int64_t wstep = (int64_t)(P.Npad8 >> 3) * 1024;
+          const uint32_t bbytes = (uint32_t)min(P.BN, P.Npad8 - nt * P.BN) * kChunkBytes;
+          for (int c = c0; c < c1; ++c) {
+            mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
+            if (lane == 0) {
+              const uint32_t fb = smem_u32(&full[ring.slot]);
+              mbar_arrive_expect_tx(fb, kAStageBytes + bbytes);
+              tma_load_2d(smem_u32(sA + ring.slot * kAStageBytes), tmap, c * ELEMS, mt * kBM, fb);
+              bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
+              mbar_arrive_cnt(fb, kProducerWarps);   // stands in for the 4 producer warps' arrivals
+              if (tfirst && c - c0 < 3) IOS_TRACE(c == c0 ? 2 : 8 + c - c0);
+            }
+            __syncwarp();
+            ring.next();
+          }
+          if (lane == 0 && tfirst) IOS_TRACE(12);
+          tfirst = false;
+        } else {
+          ring.advance(c1 - c0);
+        }
+        continue;
+      }
       // everything the chunk loop needs lives in registers: the cp.async asm statements clobber
       // "memory", which would otherwise force the descriptor fields to be re-read from smem
       const View in = views[P.in_begin];
@@ -610,7 +663,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         if (pend[0] >= 0) {
           cp_async_wait<2>();
           fence_proxy_async();
-          mbar_arrive(smem_u32(&full[pend[0]]));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&full[pend[0]]));   // one arrival per producer warp
         }
         pend[0] = pend[1];
         pend[1] = ring.slot;
@@ -620,8 +674,11 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       if (ptid == 0 && tfirst) IOS_TRACE(12);
       tfirst = false;
       fence_proxy_async();
-      if (pend[0] >= 0) mbar_arrive(smem_u32(&full[pend[0]]));
-      if (pend[1] >= 0) mbar_arrive(smem_u32(&full[pend[1]]));
+      __syncwarp();
+      if (lane == 0) {
+        if (pend[0] >= 0) mbar_arrive(smem_u32(&full[pend[0]]));
+        if (pend[1] >= 0) mbar_arrive(smem_u32(&full[pend[1]]));
+      }
     }
   } else if (warp == kMmaWarp) {
     // ============================================================== MMA ISSUER
@@ -641,6 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const int c0 = s * P.chunks_per_split;
         const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
         const uint32_t idesc = umma_idesc(DT == ET_BF16, P.BN);
+        const bool a_sw128 = P.a_tma != 0;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)acc * kMaxBN;
@@ -653,8 +711,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)   // 4 x 32 B of K per 128 B chunk
-              umma<DT>(tmem_d, umma_desc(a0 + kk * 256, 128, 1024), umma_desc(b0 + kk * 256, 128, 1024), idesc,
-                       (c > c0 || kk > 0) ? 1u : 0u);
+              umma<DT>(tmem_d, a_sw128 ? umma_desc_sw128(a0 + kk * 32) : umma_desc(a0 + kk * 256, 128, 1024),
+                       umma_desc(b0 + kk * 256, 128, 1024), idesc, (c > c0 || kk > 0) ? 1u : 0u);
             umma_commit(smem_u32(&empty[ring.slot]));
           }
           __syncwarp();
@@ -702,49 +760,69 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       named_bar(2, 128);
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       if (etid == 0 && tfirst) IOS_TRACE(5);
-      tfirst = false;
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
       const int out_tile = mt * P.n_tiles_n + nt;
       if (P.split == 1 && P.n_seg == 1) {
-        // one output segment (every non-merged GEMM): row address once, 32 columns per TMEM round
+        // one output segment (every non-merged GEMM). Per 32-column round: TMEM -> registers
+        // (thread = row) -> bias/ReLU/rounding -> this warp's 4 KB smem staging tile (16 B pieces
+        // XOR-swizzled by row: conflict-free) -> coalesced 16 B global stores (lanes sweep a row's
+        // contiguous channels; 4 rows per instruction) instead of 32 scattered rows.
         constexpr int OESZ = DT == ET_BF16 ? 2 : 4;
+        constexpr int PPR = 32 * OESZ / 16;                 // 16 B pieces per row per round (8 / 4)
         const Segment& sg = segs[P.seg_begin];
-        const int nend = sg.n1, relu = sg.relu;
-        char* orow = reinterpret_cast<char*>(sg.out.ptr) +
-                     ((int64_t)m * sg.out.cstride + sg.out.coff - sg.n0) * OESZ;
+        const int relu = sg.relu;
+        const int ncols = min(P.BN, sg.n1 - nt * P.BN);     // valid columns of this tile
+        const int wrow0 = mt * kBM + (warp & 3) * 32;       // first tile row of this warp
+        char* obase = reinterpret_cast<char*>(sg.out.ptr) +
+                      ((int64_t)sg.out.coff + nt * P.BN - sg.n0) * OESZ;
+        const int ocs = sg.out.cstride;
+        const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
         for (int c0 = 0; c0 < P.BN; c0 += 32) {
           uint32_t va[16], vb[16];
           tmem_ld16(tbase + c0, va);
           tmem_ld16(tbase + c0 + 16, vb);
           tmem_ld_wait();
-          if (!valid) continue;
+          if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(13);
+          float o[32];
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const int ncol = nt * P.BN + c0 + g * 8;
-            if (c0 + g * 8 >= P.BN || ncol >= nend) break;
-            const float4 b0 = *reinterpret_cast<const float4*>(sbias + c0 + g * 8);
-            const float4 b1 = *reinterpret_cast<const float4*>(sbias + c0 + g * 8 + 4);
-            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-            float o[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const uint32_t raw = g < 2 ? va[g * 8 + e] : vb[(g - 2) * 8 + e];
-              o[e] = __uint_as_float(raw) + bb[e];
-              if (relu) o[e] = fmaxf(o[e], 0.f);
-            }
-            if (DT == ET_BF16) {
-              uint4 pk;
-              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&pk);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
-              *reinterpret_cast<uint4*>(orow + (int64_t)ncol * OESZ) = pk;
-            } else {
-              float4* dst = reinterpret_cast<float4*>(orow + (int64_t)ncol * OESZ);
-              dst[0] = make_float4(tf32_round(o[0]), tf32_round(o[1]), tf32_round(o[2]), tf32_round(o[3]));
-              dst[1] = make_float4(tf32_round(o[4]), tf32_round(o[5]), tf32_round(o[6]), tf32_round(o[7]));
-            }
+          for (int e = 0; e < 32; ++e) {
+            o[e] = __uint_as_float(e < 16 ? va[e] : vb[e - 16]) + sbias[c0 + e];
+            if (relu) o[e] = fmaxf(o[e], 0.f);
           }
+#pragma unroll
+          for (int p = 0; p < PPR; ++p) {
+            uint32_t w[4];
+            if (DT == ET_BF16) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(o[p * 8 + 2 * q], o[p * 8 + 2 * q + 1]);
+                w[q] = *reinterpret_cast<uint32_t*>(&h);
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) w[q] = __float_as_uint(tf32_round(o[p * 4 + q]));
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * (PPR * 16) + ((p ^ (lane & 7)) % PPR) * 16),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
+          }
+          __syncwarp();
+          if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(14);
+          // coalesced write-out: lane -> (row, piece)
+          constexpr int RPI = 32 / PPR;                     // rows per instruction (4 / 8)
+#pragma unroll
+          for (int it = 0; it < 32 / RPI; ++it) {
+            const int r = it * RPI + lane / PPR, p = lane % PPR;
+            uint32_t w0, w1, w2, w3;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                         : "r"(stg + r * (PPR * 16) + ((p ^ (r & 7)) % PPR) * 16));
+            const int mrow = wrow0 + r;
+            const int col = c0 + p * (16 / OESZ);
+            if (mrow < P.M && col < ncols)
+              *reinterpret_cast<uint4*>(obase + ((int64_t)mrow * ocs + col) * OESZ) = make_uint4(w0, w1, w2, w3);
+          }
+          __syncwarp();
+          if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(15);
         }
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty[acc]));
@@ -783,18 +861,34 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // vector reductions (fire-and-forget at L2); the last arriving split reads the sum once,
         // applies bias/ReLU, stores, and re-zeroes the accumulator for the next launch.
         float* ws = reinterpret_cast<float*>(P.workspace);
-        float* mine = ws + ((int64_t)out_tile * kBM + etid) * P.BN;
-        for (int c0 = 0; c0 < P.BN; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16(tbase + c0, v);
+        float* tacc = ws + (int64_t)out_tile * kBM * P.BN;     // [kBM][BN] fp32 accumulator
+        const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
+        const int wr0 = (warp & 3) * 32;
+        for (int c0 = 0; c0 < P.BN; c0 += 32) {
+          uint32_t va[16], vb[16];
+          tmem_ld16(tbase + c0, va);
+          tmem_ld16(tbase + c0 + 16, vb);
           tmem_ld_wait();
-          if (valid) {
+          // stage (swizzled) then coalesced vector reductions: 4 rows x 128 B per instruction
 #pragma unroll
-            for (int q = 0; q < 16; q += 4)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mine + c0 + q), "r"(v[q]),
-                           "r"(v[q + 1]), "r"(v[q + 2]), "r"(v[q + 3])
-                           : "memory");
+          for (int p = 0; p < 8; ++p) {
+            const uint32_t* src = p < 4 ? va + p * 4 : vb + (p - 4) * 4;
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((p ^ (lane & 7)) * 16)),
+                         "r"(src[0]), "r"(src[1]), "r"(src[2]), "r"(src[3]) : "memory");
           }
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = it * 4 + lane / 8, p = lane % 8;
+            uint32_t w0, w1, w2, w3;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                         : "r"(stg + r * 128 + ((p ^ (r & 7)) * 16)));
+            const int col = c0 + p * 4;
+            if (mt * kBM + wr0 + r < P.M && col < P.BN)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(tacc + (wr0 + r) * P.BN + col),
+                           "r"(w0), "r"(w1), "r"(w2), "r"(w3) : "memory");
+          }
+          __syncwarp();
         }
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty[acc]));
@@ -805,9 +899,17 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         }
         named_bar(2, 128);
         const bool last = *flag != 0;
-        if (last && valid) {
-          for (int c0 = 0; c0 < P.BN; c0 += 8) {
-            const int ncol = nt * P.BN + c0;
+        if (last) {
+          // finalize the whole tile with all 128 threads, coalesced (consecutive threads sweep a
+          // row's contiguous columns), then re-zero the accumulator for the next launch
+          const int q4 = P.BN / 4;
+          const int rows = min(kBM, P.M - mt * kBM);
+          for (int idx = etid; idx < rows * q4; idx += 128) {
+            const int r = idx / q4, col = (idx - r * q4) * 4;
+            float4* src = reinterpret_cast<float4*>(tacc + r * P.BN + col);
+            const float4 x = __ldcg(src);
+            __stcg(src, make_float4(0.f, 0.f, 0.f, 0.f));
+            const int ncol = nt * P.BN + col;
             const Segment* sgp = nullptr;
             for (int q = 0; q < P.n_seg; ++q) {
               const Segment& sg = segs[P.seg_begin + q];
@@ -816,22 +918,23 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
                 break;
               }
             }
-            float4* src = reinterpret_cast<float4*>(mine + c0);
-            const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
-            __stcg(src, make_float4(0.f, 0.f, 0.f, 0.f));
-            __stcg(src + 1, make_float4(0.f, 0.f, 0.f, 0.f));
             if (!sgp) continue;
-            float o[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-            const float4 b0 = *reinterpret_cast<const float4*>(sbias + c0);
-            const float4 b1 = *reinterpret_cast<const float4*>(sbias + c0 + 4);
-            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            float o[4] = {x.x + sbias[col], x.y + sbias[col + 1], x.z + sbias[col + 2], x.w + sbias[col + 3]};
+            if (sgp->relu) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              o[e] += bb[e];
-              if (sgp->relu) o[e] = fmaxf(o[e], 0.f);
+              for (int e = 0; e < 4; ++e) o[e] = fmaxf(o[e], 0.f);
             }
-            store_vec(sgp->out, DT, m, ncol - sgp->n0, o);
-            if (DT != ET_BF16) store_vec(sgp->out, DT, m, ncol - sgp->n0 + 4, o + 4);
+            const int64_t pix = (int64_t)mt * kBM + r;
+            if (DT == ET_BF16) {
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
+              uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sgp->out.ptr) + pix * sgp->out.cstride +
+                                        sgp->out.coff + ncol - sgp->n0) = pk;
+            } else {
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(sgp->out.ptr) + pix * sgp->out.cstride +
+                                         sgp->out.coff + ncol - sgp->n0) =
+                  make_float4(tf32_round(o[0]), tf32_round(o[1]), tf32_round(o[2]), tf32_round(o[3]));
+            }
           }
         }
         if (!last) {
@@ -844,6 +947,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         named_bar(2, 128);
         if (etid == 0) red_release_add(counters + P.done_idx, 1);
       }
+      tfirst = false;
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1u;
     }
@@ -861,7 +965,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   }
   if (tid == 0) {
     IOS_TRACE(7);
-    if (sd.n_counters > 1) {
+    if (sd.uses_counters) {
       // the last CTA out resets the stage's counters for the next launch (graph-replay safe)
       const int old = atom_acqrel_add(counters, 1);
       if (old == (int)gridDim.x - 1) {

@@ -14,11 +14,11 @@ for ops, t in stages:
     buf = (C.c_uint64 * (148 * 16))()
     grid = C.c_int32()
     _check(lib.ios_stage_trace(g.handle, _i32(ops), len(ops), t, buf, 148 * 16, C.byref(grid)))
-    a = np.array(buf[:grid.value * 16], dtype=np.int64).reshape(grid.value, 16)[:, :13]
+    a = np.array(buf[:grid.value * 16], dtype=np.int64).reshape(grid.value, 16)[:, :16]
     t0 = a[:, 0][a[:, 0] > 0].min()
     rel = np.where(a > 0, (a - t0) / 1000.0, np.nan)
     print(f"stage {ops} T={t} profiled {ms*1e3:.1f} us, grid {grid.value}; us since first entry (min/median/max over CTAs):")
-    names = ["entry", "prologue", "A1 issued", "prod done", "mma done", "acc1 ready", "epi done", "teardown", "exit", "A2 issued", "A3 issued", "-", "A landed"]
+    names = ["entry", "prologue", "A1 issued", "prod done", "mma done", "acc1 ready", "epi done", "teardown", "exit", "A2 issued", "A3 issued", "-", "A landed", "e:tmem1", "e:staged1", "e:stored1"]
     for k, nm in enumerate(names):
         col = rel[:, k]
         col = col[~np.isnan(col)]
