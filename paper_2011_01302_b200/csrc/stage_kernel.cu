@@ -573,6 +573,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         } else {
           ring.advance(c1 - c0);
         }
+        // keep the four producer warps in step across a TMA tile: letting warps 1-3 run ahead into
+        // a following cp.async tile while warp 0 still issues this tile's chunks faults on the GPU
+        // (observed with a 1x1 TMA tile followed by an independent gather tile in one stage)
+        named_bar(1, 128);
         continue;
       }
       // everything the chunk loop needs lives in registers: the cp.async asm statements clobber
