@@ -7,6 +7,7 @@
 //   runner      (A9): the stages of Q in order, captured once into a CUDA graph
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -231,7 +232,28 @@ struct GemmSpec {
   int BN, ntn, mt, split, cps;
 };
 
+// Tiling knobs (env overrides are for experiments; defaults from Inception V3 b=1 sweeps)
+struct TileKnobs {
+  int target_units;   // stop refining once the stage has this many units (0 = #SMs)
+  int min_cps;        // never split K below this many 128 B chunks per unit
+  int min_bn_small;   // narrowest N tile for small-M (<= 2 m-tiles) GEMMs
+  int min_bn;         // narrowest N tile otherwise
+};
+static TileKnobs tile_knobs() {
+  static TileKnobs k = [] {
+    auto env = [](const char* n, int d) {
+      const char* v = getenv(n);
+      return v ? atoi(v) : d;
+    };
+    return TileKnobs{env("IOS_TARGET_UNITS", 0), env("IOS_MIN_CPS", 4), env("IOS_MIN_BN_SMALL", 16),
+                     env("IOS_MIN_BN", 64)};
+  }();
+  return k;
+}
+
 void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
+  const TileKnobs kn = tile_knobs();
+  const int target = kn.target_units > 0 ? kn.target_units : num_sms;
   for (GemmSpec* p : gs) {
     p->mt = (p->M + kBM - 1) / kBM;
     if (p->N16 <= kMaxBN) {
@@ -245,18 +267,18 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
     p->cps = p->kch;
   }
   // Fill the SMs: refine the problem with the most expensive tile (N halving first, then split-K)
-  // until there are about as many units as SMs.
+  // until there are about as many units as the target.
   for (int it = 0; it < 256; ++it) {
     int units = simt_tiles;
     for (GemmSpec* p : gs) units += p->mt * p->ntn * p->split;
-    if (units >= num_sms) break;
+    if (units >= target) break;
     GemmSpec* best = nullptr;
     double best_cost = 0;
     for (GemmSpec* p : gs) {
       // small-M GEMMs are weight-bound: narrow N tiles first (A is small and L2-resident), then split K
-      const int min_bn = p->mt <= 2 ? 16 : 64;
+      const int min_bn = p->mt <= 2 ? kn.min_bn_small : kn.min_bn;
       const bool can_n = p->BN >= 2 * min_bn;
-      const bool can_k = p->cps >= 4 && p->split < 32;
+      const bool can_k = p->cps >= 2 * kn.min_cps && p->split < 32;
       if (!can_n && !can_k) continue;
       const double c = p->cps * (1.0 + p->BN / 256.0);
       if (c > best_cost) {
@@ -265,7 +287,7 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       }
     }
     if (!best) break;
-    if (best->BN >= 2 * (best->mt <= 2 ? 16 : 64)) {
+    if (best->BN >= 2 * (best->mt <= 2 ? kn.min_bn_small : kn.min_bn)) {
       best->BN = round_up(best->BN / 2, 16);
       best->ntn = (best->N16 + best->BN - 1) / best->BN;
     } else {

@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   const uint32_t tmem_base = *tmem_slot;
   // programmatic dependent launch: the prologue above overlapped the previous stage's tail; from
   // here on we read activations (and counters) the previous grid may still be writing
+  if (tid == 0) IOS_TRACE(11);   // before waiting for the previous grid
   pdl_wait();
   pdl_launch_dependents();
   if (tid == 0) IOS_TRACE(1);
@@ -908,36 +909,50 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           // row's contiguous columns), then re-zero the accumulator for the next launch
           const int q4 = P.BN / 4;
           const int rows = min(kBM, P.M - mt * kBM);
-          for (int idx = etid; idx < rows * q4; idx += 128) {
-            const int r = idx / q4, col = (idx - r * q4) * 4;
-            float4* src = reinterpret_cast<float4*>(tacc + r * P.BN + col);
-            const float4 x = __ldcg(src);
-            __stcg(src, make_float4(0.f, 0.f, 0.f, 0.f));
-            const int ncol = nt * P.BN + col;
-            const Segment* sgp = nullptr;
-            for (int q = 0; q < P.n_seg; ++q) {
-              const Segment& sg = segs[P.seg_begin + q];
-              if (ncol >= sg.n0 && ncol < sg.n1) {
-                sgp = &sg;
-                break;
+          const int total = rows * q4;
+          // 8 independent float4 loads in flight per thread per round (the accumulator sits in L2)
+          for (int base = etid; base < total; base += 128 * 8) {
+            float4 x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int idx = base + u * 128;
+              if (idx < total) {
+                const int r = idx / q4, col = (idx - r * q4) * 4;
+                x[u] = __ldcg(reinterpret_cast<const float4*>(tacc + r * P.BN + col));
               }
             }
-            if (!sgp) continue;
-            float o[4] = {x.x + sbias[col], x.y + sbias[col + 1], x.z + sbias[col + 2], x.w + sbias[col + 3]};
-            if (sgp->relu) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) o[e] = fmaxf(o[e], 0.f);
-            }
-            const int64_t pix = (int64_t)mt * kBM + r;
-            if (DT == ET_BF16) {
-              __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
-              uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
-              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sgp->out.ptr) + pix * sgp->out.cstride +
-                                        sgp->out.coff + ncol - sgp->n0) = pk;
-            } else {
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(sgp->out.ptr) + pix * sgp->out.cstride +
-                                         sgp->out.coff + ncol - sgp->n0) =
-                  make_float4(tf32_round(o[0]), tf32_round(o[1]), tf32_round(o[2]), tf32_round(o[3]));
+            for (int u = 0; u < 8; ++u) {
+              const int idx = base + u * 128;
+              if (idx >= total) break;
+              const int r = idx / q4, col = (idx - r * q4) * 4;
+              __stcg(reinterpret_cast<float4*>(tacc + r * P.BN + col), make_float4(0.f, 0.f, 0.f, 0.f));
+              const int ncol = nt * P.BN + col;
+              const Segment* sgp = &segs[P.seg_begin];
+              if (P.n_seg > 1) {
+                for (int q = 0; q < P.n_seg; ++q)
+                  if (ncol >= segs[P.seg_begin + q].n0 && ncol < segs[P.seg_begin + q].n1) {
+                    sgp = &segs[P.seg_begin + q];
+                    break;
+                  }
+              }
+              if (ncol < sgp->n0 || ncol >= sgp->n1) continue;
+              float o[4] = {x[u].x + sbias[col], x[u].y + sbias[col + 1], x[u].z + sbias[col + 2], x[u].w + sbias[col + 3]};
+              if (sgp->relu) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[e] = fmaxf(o[e], 0.f);
+              }
+              const int64_t pix = (int64_t)mt * kBM + r;
+              if (DT == ET_BF16) {
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
+                uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sgp->out.ptr) + pix * sgp->out.cstride +
+                                          sgp->out.coff + ncol - sgp->n0) = pk;
+              } else {
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(sgp->out.ptr) + pix * sgp->out.cstride +
+                                           sgp->out.coff + ncol - sgp->n0) =
+                    make_float4(tf32_round(o[0]), tf32_round(o[1]), tf32_round(o[2]), tf32_round(o[3]));
+              }
             }
           }
         }
