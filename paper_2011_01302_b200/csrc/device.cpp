@@ -246,7 +246,7 @@ static TileKnobs tile_knobs() {
       return v ? atoi(v) : d;
     };
     return TileKnobs{env("IOS_TARGET_UNITS", 0), env("IOS_MIN_CPS", 4), env("IOS_MIN_BN_SMALL", 16),
-                     env("IOS_MIN_BN", 64)};
+                     env("IOS_MIN_BN", 32)};
   }();
   return k;
 }
