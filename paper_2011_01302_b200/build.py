@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("libios build failed")
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, "-shared", "-o", tmp, *objs, "-lcuda"]
+    cmd = [NVCC, *FLAGS, "-shared", "-o", tmp, *objs]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     return LIB

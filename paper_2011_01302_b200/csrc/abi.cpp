@@ -458,7 +458,7 @@ ios_status ios_schedule_launches(ios_graph gh, ios_schedule qh, int32_t* n) {
 // by the graph signature line so a cache from another graph/math/batch is rejected).
 static std::string graph_signature(const Graph& g) {
   std::ostringstream s;
-  s << "ios-latency-cache v1 batch=" << g.batch << " math=" << (int)g.math << " ops=" << g.ops.size();
+  s << "ios-latency-cache v2 batch=" << g.batch << " math=" << (int)g.math << " ops=" << g.ops.size();
   uint64_t h = 1469598103934665603ull;
   for (const Op& o : g.ops) {
     const int f[] = {o.kind, o.block, o.C, o.H, o.W, o.kh, o.kw, o.sh, o.sw, o.ph, o.pw, o.flags, (int)o.inputs.size()};
@@ -489,10 +489,10 @@ ios_status ios_latency_cache_load(ios_graph gh, const char* path) {
   std::string sig;
   std::getline(f, sig);
   if (sig != graph_signature(gh->g)) IOS_FAIL(IOS_ERR_INVALID_ARG, "latency cache belongs to another graph");
-  int bp, t;
-  unsigned long long m;
+  unsigned long long bsig, m;
+  int t;
   double v;
-  while (f >> bp >> m >> t >> v) gh->g.latency_cache[std::make_tuple(bp, (uint64_t)m, t)] = v;
+  while (f >> bsig >> m >> t >> v) gh->g.latency_cache[std::make_tuple((uint64_t)bsig, (uint64_t)m, t)] = v;
   ABI_END
 }
 

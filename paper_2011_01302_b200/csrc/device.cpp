@@ -46,6 +46,7 @@ struct StagePlan {
   void* workspace = nullptr;
   void* merged_pack = nullptr;
   float* merged_bias = nullptr;
+  std::vector<void*> allocs;  // pool allocations owned by this plan
 };
 
 struct DeviceState {
@@ -63,19 +64,34 @@ struct DeviceState {
 
 namespace {
 
-void* dmalloc(DeviceState& d, size_t bytes) {
+// Persistent graph memory (activations, weights) is cudaMalloc'ed and lives with the graph.
+// Stage-plan memory (`owner` != nullptr) comes from the stream-ordered pool so the profiler can
+// build, measure and drop hundreds of thousands of candidate stages cheaply.
+void* dmalloc(DeviceState& d, size_t bytes, std::vector<void*>* owner = nullptr) {
   void* p = nullptr;
-  IOS_CHECK_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
-  IOS_CHECK_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 256)));
-  d.allocs.push_back(p);
+  bytes = std::max<size_t>(bytes, 256);
+  if (owner) {
+    IOS_CHECK_CUDA(cudaMallocAsync(&p, bytes, d.stream));
+    IOS_CHECK_CUDA(cudaMemsetAsync(p, 0, bytes, d.stream));
+    owner->push_back(p);
+  } else {
+    IOS_CHECK_CUDA(cudaMalloc(&p, bytes));
+    IOS_CHECK_CUDA(cudaMemset(p, 0, bytes));
+    d.allocs.push_back(p);
+  }
   return p;
 }
 
 template <class T>
-T* upload(DeviceState& d, const std::vector<T>& v, size_t min_elems = 0) {
+T* upload(DeviceState& d, const std::vector<T>& v, size_t min_elems = 0, std::vector<void*>* owner = nullptr) {
   const size_t n = std::max(v.size(), min_elems);
-  T* p = static_cast<T*>(dmalloc(d, n * sizeof(T)));
-  if (!v.empty()) IOS_CHECK_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  T* p = static_cast<T*>(dmalloc(d, n * sizeof(T), owner));
+  if (!v.empty()) {
+    if (owner)
+      IOS_CHECK_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, d.stream));
+    else
+      IOS_CHECK_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
   return p;
 }
 
@@ -98,7 +114,7 @@ uint16_t bf16_rne_bits(float x) {
 // order: [k chunk][n / 8][8 pieces of 16 B][n % 8][16 B]. Any BN rows starting at a multiple of 8
 // of one chunk are then one contiguous run of BN * 128 bytes (one cp.async.bulk).
 template <class F>
-void* pack_gemm(DeviceState& d, int N, int K, bool bf16, F w, int* n8_out) {
+void* pack_gemm(DeviceState& d, int N, int K, bool bf16, F w, int* n8_out, std::vector<void*>* owner = nullptr) {
   const int esz = bf16 ? 2 : 4, elems = kChunkBytes / esz, vec = 16 / esz;
   const int kch = (K + elems - 1) / elems;
   const int n8 = round_up(N, 8);
@@ -119,7 +135,7 @@ void* pack_gemm(DeviceState& d, int N, int K, bool bf16, F w, int* n8_out) {
     }
   }
   *n8_out = n8;
-  return upload(d, buf);
+  return upload(d, buf, 0, owner);
 }
 
 int64_t view_elems(const Op& o, int C) { return (int64_t)o.N * o.H * o.W * C; }
@@ -138,6 +154,13 @@ void ensure_device(Graph& g) {
     IOS_FAIL(IOS_ERR_CUDA, std::string("libios is built for sm_100a; device is ") + prop.name);
   d.num_sms = prop.multiProcessorCount;
   IOS_CHECK_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, g.device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   IOS_CHECK_CUDA(cudaEventCreate(&d.ev0));
   IOS_CHECK_CUDA(cudaEventCreate(&d.ev1));
   d.err = static_cast<int*>(dmalloc(d, 16));
@@ -389,6 +412,30 @@ struct PlanBuilder {
   }
 };
 
+// The driver's tensor-map encoder, resolved through the runtime (no link-time libcuda dependency:
+// the library must load on machines without a driver).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  if (!fn) IOS_FAIL(IOS_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  return fn;
+}
+
+void free_plan(DeviceState& d, StagePlan* p) {
+  if (!p) return;
+  for (void* a : p->allocs) cudaFreeAsync(a, d.stream);
+  delete p;
+}
+
 StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
   DeviceState& d = *g.dev;
   const std::vector<int> ops = g.ops_of(bpos, mask);
@@ -427,13 +474,13 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
         const int i = tap / KW - (-o.ph - st_h), j = tap % KW - (-o.pw - st_w);
         if (i < 0 || i >= o.kh || j < 0 || j >= o.kw) return 0.0f;
         return o.weight[(((size_t)r * cin + ci) * o.kh + i) * o.kw + j];
-      }, &merged_n8);
+      }, &merged_n8, &plan->allocs);
       std::vector<float> bias((size_t)round_up(ntot, 256) + 16, 0.0f);
       for (size_t bi = 0; bi < ops.size(); ++bi) {
         const Op& o = g.ops[ops[bi]];
         for (int c = 0; c < o.cout; ++c) bias[row0[bi] + c] = o.bias[c];
       }
-      plan->merged_bias = upload(d, bias);
+      plan->merged_bias = upload(d, bias, 0, &plan->allocs);
       const int pi = b.gemm(f.inputs[0], d.od[f.inputs[0]].out, plan->merged_pack, merged_n8, plan->merged_bias,
                             ntot, KH, KW, f.sh, f.sw, PH, PW, f.H, f.W, f.flags & IOS_F_RELU_PRE);
       for (size_t bi = 0; bi < ops.size(); ++bi) {
@@ -569,7 +616,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
     }
     plan->empty = tiles == 0;
     if (!plan->empty) {
-      if (ws_bytes) plan->workspace = dmalloc(d, ws_bytes);
+      if (ws_bytes) plan->workspace = dmalloc(d, ws_bytes, &plan->allocs);
       for (Problem& p : b.probs)
         if (p.kind == PK_GEMM && p.split > 1) p.workspace += (uint64_t)plan->workspace;
       const size_t pb = b.probs.size() * sizeof(Problem), vb = b.views.size() * sizeof(View),
@@ -592,7 +639,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
         const cuuint32_t box[2] = {(cuuint32_t)(kChunkBytes / g.esize()), (cuuint32_t)kBM};
         const cuuint32_t estr[2] = {1, 1};
         void* base = reinterpret_cast<char*>(in.ptr) + (size_t)in.coff * g.esize();
-        CUresult r = cuTensorMapEncodeTiled(&tm, g.math == IOS_MATH_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+        CUresult r = encode_tiled()(&tm, g.math == IOS_MATH_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                             2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -605,14 +652,13 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
         maps.push_back(tm);
       }
       if (!maps.empty()) {
-        void* mp = dmalloc(d, maps.size() * sizeof(CUtensorMap));
-        IOS_CHECK_CUDA(cudaMemcpy(mp, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+        void* mp = upload(d, maps, 0, &plan->allocs);
         for (Problem& p : b.probs)
           if (p.kind == PK_GEMM && p.a_tma) p.tmap_a = (uint64_t)mp + p.tmap_a * sizeof(CUtensorMap);
       }
       std::memcpy(blob.data(), b.probs.data(), pb);
-      plan->dmem = upload(d, blob);
-      plan->counters = static_cast<int*>(dmalloc(d, (size_t)n_counters * sizeof(int)));
+      plan->dmem = upload(d, blob, 0, &plan->allocs);
+      plan->counters = static_cast<int*>(dmalloc(d, (size_t)n_counters * sizeof(int), &plan->allocs));
       StageDesc& sd = plan->sd;
       sd.problems = (uint64_t)plan->dmem;
       sd.views = (uint64_t)plan->dmem + pb;
@@ -633,7 +679,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       plan->dtype = g.dtype();
     }
   } catch (...) {
-    delete plan;
+    free_plan(d, plan);
     throw;
   }
   return plan;
@@ -674,14 +720,32 @@ double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const 
   const int trials = opts && opts->trials > 0 ? opts->trials : 5;
   const int reps = opts && opts->reps > 0 ? opts->reps : 20;
   const bool flush = opts && opts->l2_flush;
+  // measure with the cached plan if a run already built one, else with a transient plan that is
+  // dropped afterwards (the DP measures each distinct stage once; ios_run rebuilds what it needs)
+  const auto key = std::make_tuple(g.block_sig(bpos), mask, strategy);
   StagePlan* p;
+  bool transient = false;
+  auto pit = d.plans.find(std::make_tuple(bpos, mask, strategy));
   try {
-    p = get_plan(g, bpos, mask, strategy);
+    if (pit != d.plans.end()) {
+      p = pit->second;
+    } else {
+      p = build_plan(g, bpos, mask, strategy);
+      transient = true;
+    }
   } catch (const Error& e) {
     if (e.code != IOS_ERR_UNSUPPORTED) throw;
-    g.latency_cache[std::make_tuple(bpos, mask, strategy)] = kInf;   // not executable -> never chosen
+    g.latency_cache[key] = kInf;   // not executable -> never chosen
     return kInf;
   }
+  struct Drop {
+    DeviceState& d;
+    StagePlan* p;
+    bool on;
+    ~Drop() {
+      if (on) free_plan(d, p);
+    }
+  } drop{d, p, transient};
   double ms = 0.0;
   if (!p->empty) {
     if (flush && !d.l2buf) d.l2buf = dmalloc(d, (size_t)d.l2bytes);
@@ -701,7 +765,7 @@ double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const 
     std::sort(t.begin(), t.end());
     ms = t[t.size() / 2];
   }
-  g.latency_cache[std::make_tuple(bpos, mask, strategy)] = ms;
+  g.latency_cache[key] = ms;
   return ms;
 }
 
@@ -795,7 +859,8 @@ void destroy_schedule_exec(Schedule& q) {
 void destroy_device(Graph& g) {
   if (!g.dev) return;
   DeviceState& d = *g.dev;
-  for (auto& [k, p] : d.plans) delete p;
+  for (auto& [k, p] : d.plans) free_plan(d, p);
+  if (d.stream) cudaStreamSynchronize(d.stream);
   for (void* p : d.allocs) cudaFree(p);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);

@@ -154,7 +154,7 @@ double schedule_dp(Graph& g, int r, int s, int set, ios_cost_fn cost, void* ctx,
         ++n_costed;
         return v;
       }
-      auto key = std::make_tuple(bp, mask, t);
+      auto key = std::make_tuple(g.block_sig(bp), mask, t);
       auto it = g.latency_cache.find(key);
       if (it != g.latency_cache.end()) return it->second;
       // search-time profile: fewer repetitions than ios_stage_latency's defaults (Z15); the DP

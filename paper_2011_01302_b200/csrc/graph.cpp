@@ -118,6 +118,36 @@ void validate_schedule(const Graph& g, const Schedule& q) {
     }
 }
 
+// Structural hash of a block: op kinds, hyper-parameters, output shapes, in-block edges (as local
+// indices) and the shapes of external inputs. Stage latency depends on these, not on weights.
+uint64_t Graph::block_sig(int bpos) {
+  if (block_sigs.size() != blocks.size()) block_sigs.assign(blocks.size(), 0);
+  if (block_sigs[bpos]) return block_sigs[bpos];
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](int64_t v) { h = (h ^ (uint64_t)v) * 1099511628211ull; };
+  mix(batch);
+  mix((int)math);
+  for (int v : blocks[bpos].ops) {
+    const Op& o = ops[v];
+    for (int64_t x : {(int64_t)o.kind, (int64_t)o.C, (int64_t)o.H, (int64_t)o.W, (int64_t)o.kh, (int64_t)o.kw,
+                      (int64_t)o.sh, (int64_t)o.sw, (int64_t)o.ph, (int64_t)o.pw, (int64_t)o.flags,
+                      (int64_t)o.inputs.size()})
+      mix(x);
+    for (int u : o.inputs) {
+      if (u != 0 && op_block_pos[u] == bpos) {
+        mix(1000000 + op_local[u]);
+      } else {
+        mix(ops[u].C);
+        mix(ops[u].H);
+        mix(ops[u].W);
+      }
+    }
+  }
+  if (h == 0) h = 1;
+  block_sigs[bpos] = h;
+  return h;
+}
+
 int pool_out_size(int h, int k, int s, int p, bool ceil_mode) { return pool_out(h, k, s, p, ceil_mode); }
 const char* last_error_cstr() { return g_last_error.c_str(); }
 

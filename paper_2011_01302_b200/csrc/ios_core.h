@@ -61,8 +61,11 @@ struct Graph {
   std::vector<BlockInfo> blocks;
   std::unordered_map<int, int> block_pos;    // block id -> index in `blocks`
   std::vector<int> op_block_pos, op_local;   // per op: block position, local index
-  // stage-latency cache: key (block pos, mask, strategy)
-  std::map<std::tuple<int, uint64_t, int>, double> latency_cache;
+  // stage-latency cache: key (block signature, mask, strategy); identical blocks (e.g. repeated
+  // NASNet cells) share their measurements
+  std::map<std::tuple<uint64_t, uint64_t, int>, double> latency_cache;
+  std::vector<uint64_t> block_sigs;   // lazily computed
+  uint64_t block_sig(int bpos);
   DeviceState* dev = nullptr;
   ~Graph();
 
