@@ -769,6 +769,79 @@ double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const 
   return ms;
 }
 
+// Search-time profiling (Z15, batched): per batch of up to 48 transient plans, one warm-up launch
+// each, then `trials` rounds of `reps` back-to-back launches per plan between CUDA events, a
+// single host sync per batch; median over rounds of the per-launch mean.
+void measure_stages(Graph& g, int bpos, const std::vector<std::pair<uint64_t, int>>& stages) {
+  if (stages.empty()) return;
+  ensure_device(g);
+  DeviceState& d = *g.dev;
+  constexpr int kBatch = 48, kTrials = 3, kReps = 3;
+  const uint64_t sig = g.block_sig(bpos);
+  std::vector<cudaEvent_t> ev;
+  auto event = [&](size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      IOS_CHECK_CUDA(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    return ev[i];
+  };
+  struct Guard {
+    std::vector<cudaEvent_t>& ev;
+    ~Guard() {
+      for (auto e : ev) cudaEventDestroy(e);
+    }
+  } guard{ev};
+  for (size_t b0 = 0; b0 < stages.size(); b0 += kBatch) {
+    const size_t b1 = std::min(stages.size(), b0 + kBatch);
+    std::vector<StagePlan*> plans(b1 - b0, nullptr);
+    struct Drop {
+      DeviceState& d;
+      std::vector<StagePlan*>& ps;
+      ~Drop() {
+        for (auto* p : ps) free_plan(d, p);
+      }
+    } drop{d, plans};
+    for (size_t i = b0; i < b1; ++i) {
+      const auto& [mask, t] = stages[i];
+      try {
+        plans[i - b0] = build_plan(g, bpos, mask, t);
+      } catch (const Error& e) {
+        if (e.code != IOS_ERR_UNSUPPORTED) throw;
+        g.latency_cache[std::make_tuple(sig, mask, t)] = kInf;
+      }
+    }
+    for (auto* p : plans)
+      if (p) launch_plan(p, d.stream);   // warm-up
+    for (int tr = 0; tr < kTrials; ++tr)
+      for (size_t i = 0; i < plans.size(); ++i) {
+        if (!plans[i] || plans[i]->empty) continue;
+        IOS_CHECK_CUDA(cudaEventRecord(event(2 * (tr * kBatch + i)), d.stream));
+        for (int r = 0; r < kReps; ++r) launch_plan(plans[i], d.stream);
+        IOS_CHECK_CUDA(cudaEventRecord(event(2 * (tr * kBatch + i) + 1), d.stream));
+      }
+    IOS_CHECK_CUDA(cudaStreamSynchronize(d.stream));
+    check_err(d);
+    for (size_t i = 0; i < plans.size(); ++i) {
+      if (!plans[i]) continue;
+      const auto& [mask, t] = stages[b0 + i];
+      double ms = 0.0;
+      if (!plans[i]->empty) {
+        std::vector<double> v;
+        for (int tr = 0; tr < kTrials; ++tr) {
+          float e = 0;
+          IOS_CHECK_CUDA(cudaEventElapsedTime(&e, ev[2 * (tr * kBatch + i)], ev[2 * (tr * kBatch + i) + 1]));
+          v.push_back((double)e / kReps);
+        }
+        std::sort(v.begin(), v.end());
+        ms = v[v.size() / 2];
+      }
+      g.latency_cache[std::make_tuple(sig, mask, t)] = ms;
+    }
+  }
+}
+
 int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* out, int cap) {
   ensure_device(g);
   DeviceState& d = *g.dev;

@@ -164,6 +164,26 @@ double schedule_dp(Graph& g, int r, int s, int set, ios_cost_fn cost, void* ctx,
       ++n_costed;
       return v;   // stage_latency fills the cache
     };
+    if (!cost) {
+      // device costs: first walk the DP with placeholder costs to collect every (mask, T) it will
+      // ask for (the search is exhaustive over endings, so the set does not depend on the costs),
+      // then measure all uncached ones in batches (one host sync per batch), then run the DP
+      std::vector<std::pair<uint64_t, int>> need;
+      std::map<std::pair<uint64_t, int>, char> seen;
+      auto collect = [&](uint64_t mask, int t) -> double {
+        auto key = std::make_pair(mask, t);
+        if (!seen.count(key)) {
+          seen[key] = 1;
+          if (!g.latency_cache.count(std::make_tuple(g.block_sig(bp), mask, t))) need.push_back(key);
+        }
+        return 1.0 + popcount64(mask);
+      };
+      BlockDP probe(g, bp, r, s, set, collect);
+      std::vector<std::pair<uint64_t, int>> q0;
+      probe.run(&q0);
+      measure_stages(g, bp, need);
+      n_costed += (int64_t)need.size();
+    }
     BlockDP dp(g, bp, r, s, set, fn);
     std::vector<std::pair<uint64_t, int>> q;
     const double c = dp.run(&q);

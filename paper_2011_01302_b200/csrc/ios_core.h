@@ -101,6 +101,8 @@ void validate_schedule(const Graph& g, const Schedule& q);   // throws BAD_SCHED
 
 // ------------------------------------------------------------------------------------ device
 double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const ios_profile_opts* opts);
+// Batch measurement for the DP's search (fills g.latency_cache for every (mask, strategy) of block bpos)
+void measure_stages(Graph& g, int bpos, const std::vector<std::pair<uint64_t, int>>& stages);
 void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStream_t st);
 void op_output(Graph& g, int op, void* d_out, cudaStream_t st);
 int schedule_launches(Graph& g, Schedule& q);
