@@ -142,7 +142,19 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     spec = NETS[args.net]
-    net = W.build(args.net, math=spec["math"])
+    # batch sharding: contiguous per-rank slices, each rank its own graph + DP schedule;
+    # batch 1 does not shard: every rank runs a batch-1 replica
+    from paper_2011_01302_b200.shard import shard_range
+    if args.batch > 1:
+        b0, b1 = shard_range(args.batch, world, rank)
+        local_batch = b1 - b0
+        parallelism = f"batch-sharded {args.batch} over {world} GPU(s) ({local_batch}/rank), no collective on the hot path"
+        images = args.batch
+    else:
+        local_batch = 1
+        parallelism = f"replicas x{world} (batch 1 does not shard)"
+        images = world
+    net = W.build(args.net, math=spec["math"], batch=local_batch)
     peaks = _peaks()
 
     g = Graph.from_netspec(net, spec["math"], local)
@@ -250,14 +262,14 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "bf16" if net.math == "bf16" else "tf32",
             "data": "synthetic (seeded N(0,1) input, He-init weights, DESIGN.md input recipe)",
-            "config": {"workload": spec["desc"], "net": args.net, "batch": 1, "schedule": f"IOS-Both r={args.r} s={args.s}",
-                       "parallelism": f"replicas x{world} (batch 1 does not shard)", "l2": "flushed before every timed step",
+            "config": {"workload": spec["desc"], "net": args.net, "batch": args.batch, "schedule": f"IOS-Both r={args.r} s={args.s}",
+                       "parallelism": parallelism, "l2": "flushed before every timed step",
                        "stages": len(q_ios.stages), "launches_per_run": launches_per_run},
             "sequential_ms": round(ms_seq, 4),
             "greedy_ms": round(ms_greedy, 4),
             "speedup_vs_sequential": round(ms_seq / ms_ios, 3),
             "speedup_vs_greedy": round(ms_greedy / ms_ios, 3),
-            "images_per_s": round(world * 1000.0 / ms_ios, 1),
+            "images_per_s": round(images * 1000.0 / ms_ios, 1),
             "search_s": round(search_s, 2),
             "search_stats": {"states": q_ios.stats[0], "transitions": q_ios.stats[1], "stages_measured": q_ios.stats[2]},
             "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": unit,
@@ -325,7 +337,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": round(ms, 2), "unit": "ms", "n_gpus": world,
             "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": round(ms, 2), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": spec["desc"], "net": args.net, "batch": 1, "schedule": "sequential (oracle)"},
+            "config": {"workload": spec["desc"], "net": args.net, "batch": args.batch, "schedule": "sequential (oracle)"},
             "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": "oracle",
                              "sample": f"{steps} full batch-1 inference(s), float64 NumPy"},
             "e2e": {"value": round(ms, 2), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -338,6 +350,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--net", default="inception_v3", choices=sorted(NETS))
+    ap.add_argument("--batch", type=int, default=1, help="global batch (> 1: sharded across the ranks)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--r", type=int, default=3)
     ap.add_argument("--s", type=int, default=8)

@@ -251,9 +251,18 @@ void ensure_device(Graph& g) {
 
 // ------------------------------------------------------------------------------ stage planning
 struct GemmSpec {
-  int M, N16, K, kch;
+  int M, N16, K, kch, Npad8;
   int BN, ntn, mt, split, cps;
+  int swap;   // swap-AB: weights are the 128-row MMA operand, the (<= 128) pixels are N
 };
+
+bool swap_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("IOS_SWAP_AB");
+    return v ? atoi(v) != 0 : true;
+  }();
+  return on;
+}
 
 // Tiling knobs (env overrides are for experiments; defaults from Inception V3 b=1 sweeps)
 struct TileKnobs {
@@ -278,6 +287,15 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
   const TileKnobs kn = tile_knobs();
   const int target = kn.target_units > 0 ? kn.target_units : num_sms;
   for (GemmSpec* p : gs) {
+    if (p->swap) {
+      // swap-AB: MMA M = 128 output channels (weight rows), MMA N = all pixels, one pixel tile
+      p->BN = round_up(p->M, 16);
+      p->ntn = 1;
+      p->mt = (p->Npad8 + kBM - 1) / kBM;
+      p->split = 1;
+      p->cps = p->kch;
+      continue;
+    }
     p->mt = (p->M + kBM - 1) / kBM;
     if (p->N16 <= kMaxBN) {
       p->BN = p->N16;
@@ -300,7 +318,7 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
     for (GemmSpec* p : gs) {
       // small-M GEMMs are weight-bound: narrow N tiles first (A is small and L2-resident), then split K
       const int min_bn = p->mt <= 2 ? kn.min_bn_small : kn.min_bn;
-      const bool can_n = p->BN >= 2 * min_bn;
+      const bool can_n = !p->swap && p->BN >= 2 * min_bn;
       const bool can_k = p->cps >= 2 * kn.min_cps && p->split < 32;
       if (!can_n && !can_k) continue;
       const double c = p->cps * (1.0 + p->BN / 256.0);
@@ -310,7 +328,7 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       }
     }
     if (!best) break;
-    if (best->BN >= 2 * (best->mt <= 2 ? kn.min_bn_small : kn.min_bn)) {
+    if (!best->swap && best->BN >= 2 * (best->mt <= 2 ? kn.min_bn_small : kn.min_bn)) {
       best->BN = round_up(best->BN / 2, 16);
       best->ntn = (best->N16 + best->BN - 1) / best->BN;
     } else {
@@ -382,6 +400,8 @@ struct PlanBuilder {
     p.k_chunks = (p.K + elems - 1) / elems;
     p.seg_begin = (int)segs.size();
     GemmSpec& s = specs[pi];
+    s.Npad8 = n8;
+    s.swap = (p.M <= kBM && swap_enabled()) ? 1 : 0;
     s.M = p.M;
     s.N16 = round_up(Ntot, 16);
     s.K = p.K;
@@ -582,6 +602,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       // A via TMA when it is a plain [M, C] matrix: 1x1, stride 1, no padding, no pre-ReLU
       p.a_tma = (p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 && p.pw == 0 &&
                  !(p.flags & IOS_F_RELU_PRE)) ? 1 : 0;
+      p.swap_ab = s.swap;
       p.BN = s.BN;
       p.n_tiles_n = s.ntn;
       p.m_tiles = s.mt;

@@ -90,7 +90,10 @@ struct Problem {
   FastDiv fd_howo, fd_wo, fd_split, fd_ntn, fd_cin, fd_kw;   // divisors of the tile / im2col decode
   // SIMT geometry
   int32_t items_per_tile, n_items;  // items = output pixels (x channel vectors handled inside)
-  int32_t a_tma;                    // 1: A is a plain [M, C] matrix (1x1 s1 conv) loaded by TMA
+  int32_t a_tma;                    // 1: the activation operand is a plain [M, C] matrix loaded by TMA
+  int32_t swap_ab;                  // 1: weights are the MMA A operand (128 output channels per tile),
+                                    //    the M (<= 128) pixels are MMA N = BN; m_tiles count channel tiles
+  int32_t pad2_;
   uint64_t tmap_a;                  // global address of its CUtensorMap (2D tiled, 128B swizzle)
 };
 

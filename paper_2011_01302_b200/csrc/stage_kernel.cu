@@ -553,16 +553,23 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // issued by one thread; warps 1-3 only keep their ring position in step.
         if (warp == 0) {
           const uint64_t tmap = P.tmap_a;
-          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)nt * (P.BN >> 3) * 1024;
+          const bool swap = P.swap_ab != 0;
+          // weights: BN rows of tile nt into the B slot, or (swap-AB) 128 rows of tile mt into A
+          const int wrow0 = swap ? mt * kBM : nt * P.BN, wrows = swap ? kBM : P.BN;
+          const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)(wrow0 >> 3) * 1024;
           const int64_t wstep = (int64_t)(P.Npad8 >> 3) * 1024;
-          const uint32_t bbytes = (uint32_t)min(P.BN, P.Npad8 - nt * P.BN) * kChunkBytes;
+          const uint32_t bbytes = (uint32_t)min(wrows, P.Npad8 - wrow0) * kChunkBytes;
+          uint8_t* const wbuf = swap ? sA : sB;
+          uint8_t* const xbuf = swap ? sB : sA;
+          const int wsb = swap ? kAStageBytes : kBStageBytes, xsb = swap ? kBStageBytes : kAStageBytes;
+          const int xrow0 = swap ? 0 : mt * kBM;
           for (int c = c0; c < c1; ++c) {
             mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
             if (lane == 0) {
               const uint32_t fb = smem_u32(&full[ring.slot]);
               mbar_arrive_expect_tx(fb, kAStageBytes + bbytes);
-              tma_load_2d(smem_u32(sA + ring.slot * kAStageBytes), tmap, c * ELEMS, mt * kBM, fb);
-              bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
+              tma_load_2d(smem_u32(xbuf + ring.slot * xsb), tmap, c * ELEMS, xrow0, fb);
+              bulk_g2s(smem_u32(wbuf + ring.slot * wsb), wsrc + c * wstep, bbytes, fb);
               mbar_arrive_cnt(fb, kProducerWarps);   // stands in for the 4 producer warps' arrivals
               if (tfirst && c - c0 < 3) IOS_TRACE(c == c0 ? 2 : 8 + c - c0);
             }
@@ -586,10 +593,11 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const int inC = in.C, inH = in.H, inW = in.W, cstride = in.cstride;
       const int kh = P.kh, kw = P.kw;
       const bool relu_pre = (P.flags & 2) != 0;
+      const bool swap = P.swap_ab != 0;
       int roff[4], ih0[4], iw0[4];   // row pixel offset (may be negative: padding) and window origin
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int m = mt * kBM + (warp + 4 * j) * 8 + rig;
+        const int m = (swap ? 0 : mt * kBM) + (warp + 4 * j) * 8 + rig;
         const int n = fdiv(P.fd_howo, m);
         const int rem = m - n * (P.Ho * P.Wo);
         const int oh = fdiv(P.fd_wo, rem);
@@ -608,11 +616,16 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         ti[h] = fdiv(P.fd_kw, tap);
         tj[h] = tap - ti[h] * kw;
       }
-      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)nt * (P.BN >> 3) * 1024;
+      // weights: BN rows of n tile nt (B slot), or with swap-AB 128 rows of channel tile mt (A slot);
+      // the last tile may run past the packed rows: copy only those (the rest of the smem tile is
+      // stale and only feeds accumulator rows/columns that no output segment covers)
+      const int wrow0 = swap ? mt * kBM : nt * P.BN, wrows = swap ? kBM : P.BN;
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)(wrow0 >> 3) * 1024;
       const int64_t wstep = (int64_t)(P.Npad8 >> 3) * 1024;
-      // the last n tile may run past the packed rows: copy only those (the rest of the smem tile is
-      // stale and only feeds accumulator columns that no output segment covers)
-      const uint32_t bbytes = (uint32_t)min(P.BN, P.Npad8 - nt * P.BN) * kChunkBytes;
+      const uint32_t bbytes = (uint32_t)min(wrows, P.Npad8 - wrow0) * kChunkBytes;
+      uint8_t* const wbuf = swap ? sA : sB;
+      uint8_t* const xbuf = swap ? sB : sA;
+      const int wsb = swap ? kAStageBytes : kBStageBytes, xsb = swap ? kBStageBytes : kAStageBytes;
       const char* ibase = reinterpret_cast<const char*>(in.ptr) + (int64_t)in.coff * ESZ;
       int pend[2] = {-1, -1};
       for (int c = c0; c < c1; ++c) {
@@ -620,9 +633,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         if (ptid == 0) {
           const uint32_t fb = smem_u32(&full[ring.slot]);
           mbar_arrive_expect_tx(fb, bbytes);
-          bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
+          bulk_g2s(smem_u32(wbuf + ring.slot * wsb), wsrc + c * wstep, bbytes, fb);
         }
-        const uint32_t a_st = smem_u32(sA + ring.slot * kAStageBytes) + rig * 16 + pc0 * 128;
+        const uint32_t a_st = smem_u32(xbuf + ring.slot * xsb) + rig * 16 + pc0 * 128;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const bool kvalid = ti[h] < kh;                            // k < K
@@ -703,7 +716,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const int c0 = s * P.chunks_per_split;
         const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
         const uint32_t idesc = umma_idesc(DT == ET_BF16, P.BN);
-        const bool a_sw128 = P.a_tma != 0;
+        // the activation operand is 128 B-swizzled when TMA loads it; swap-AB puts it in the B slot
+        const bool a_sw128 = P.a_tma != 0 && !P.swap_ab;
+        const bool b_sw128 = P.a_tma != 0 && P.swap_ab;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)acc * kMaxBN;
@@ -717,7 +732,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)   // 4 x 32 B of K per 128 B chunk
               umma<DT>(tmem_d, a_sw128 ? umma_desc_sw128(a0 + kk * 32) : umma_desc(a0 + kk * 256, 128, 1024),
-                       umma_desc(b0 + kk * 256, 128, 1024), idesc, (c > c0 || kk > 0) ? 1u : 0u);
+                       b_sw128 ? umma_desc_sw128(b0 + kk * 32) : umma_desc(b0 + kk * 256, 128, 1024), idesc,
+                       (c > c0 || kk > 0) ? 1u : 0u);
             umma_commit(smem_u32(&empty[ring.slot]));
           }
           __syncwarp();
@@ -758,6 +774,103 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const bool valid = m < P.M;
       const int esz_out = P.dtype == ET_BF16 ? 2 : 4;
       const float* bias = reinterpret_cast<const float*>(P.bias);
+      if (P.swap_ab) {
+        // swap-AB tile: TMEM lane = output channel, columns = pixels. Each thread owns one channel;
+        // a warp's stores/reductions for one pixel cover 32 consecutive channels (coalesced).
+        const int ch = mt * kBM + etid;   // column of the (merged) GEMM
+        const Segment* sgp = nullptr;
+        for (int q = 0; q < P.n_seg; ++q) {
+          const Segment& sg = segs[P.seg_begin + q];
+          if (ch >= sg.n0 && ch < sg.n1) sgp = &sg;
+        }
+        const float bv = sgp ? __ldg(bias + ch) : 0.f;
+        const int relu = sgp ? sgp->relu : 0;
+        char* ocol = sgp ? reinterpret_cast<char*>(sgp->out.ptr) +
+                               ((int64_t)sgp->out.coff + ch - sgp->n0) * (DT == ET_BF16 ? 2 : 4)
+                         : nullptr;
+        const int64_t ostride = sgp ? (int64_t)sgp->out.cstride * (DT == ET_BF16 ? 2 : 4) : 0;
+        mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+        if (etid == 0 && tfirst) IOS_TRACE(5);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
+        const int out_tile = mt;
+        if (P.split == 1) {
+          for (int c0 = 0; c0 < P.BN; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tbase + c0, v);
+            tmem_ld_wait();
+            if (!sgp) continue;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int px = c0 + j;
+              if (px >= P.M) break;
+              float o = __uint_as_float(v[j]) + bv;
+              if (relu) o = fmaxf(o, 0.f);
+              if (DT == ET_BF16)
+                *reinterpret_cast<__nv_bfloat16*>(ocol + px * ostride) = __float2bfloat16_rn(o);
+              else
+                *reinterpret_cast<float*>(ocol + px * ostride) = tf32_round(o);
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(smem_u32(&tempty[acc]));
+        } else {
+          // split-K: fp32 accumulator [pixel][128 channels]; coalesced scalar reductions
+          float* tacc = reinterpret_cast<float*>(P.workspace) + (int64_t)out_tile * kBM * P.BN;
+          for (int c0 = 0; c0 < P.BN; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tbase + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int px = c0 + j;
+              if (px < P.M)
+                asm volatile("red.global.add.f32 [%0], %1;" ::"l"(tacc + px * kBM + etid), "r"(v[j]) : "memory");
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(smem_u32(&tempty[acc]));
+          named_bar(2, 128);
+          if (etid == 0) {
+            const int old = atom_acqrel_add(counters + P.tilectr_idx + out_tile, 1);
+            *flag = (old == P.split - 1);
+          }
+          named_bar(2, 128);
+          if (*flag == 0) {
+            tfirst = false;
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1u;
+            continue;
+          }
+          for (int p0 = 0; p0 < P.M; p0 += 8) {
+            float x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (p0 + u < P.M) x[u] = __ldcg(tacc + (p0 + u) * kBM + etid);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int px = p0 + u;
+              if (px >= P.M) break;
+              __stcg(tacc + px * kBM + etid, 0.f);
+              if (!sgp) continue;
+              float o = x[u] + bv;
+              if (relu) o = fmaxf(o, 0.f);
+              if (DT == ET_BF16)
+                *reinterpret_cast<__nv_bfloat16*>(ocol + px * ostride) = __float2bfloat16_rn(o);
+              else
+                *reinterpret_cast<float*>(ocol + px * ostride) = tf32_round(o);
+            }
+          }
+        }
+        if (P.signal) {
+          named_bar(2, 128);
+          if (etid == 0) red_release_add(counters + P.done_idx, 1);
+        }
+        tfirst = false;
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1u;
+        continue;
+      }
       // stage this tile's bias slice in smem while the MMAs run (one load round trip, off the
       // critical path); the previous tile's readers of this buffer are past the barrier below
       float* sbias = sbias_all + acc * kMaxBN;
