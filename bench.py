@@ -161,6 +161,8 @@ def run_ours(args):
     t0 = time.time()
     if args.latency_cache and os.path.exists(args.latency_cache):
         g.load_latency_cache(args.latency_cache)              # resume: measured stage latencies
+    if args.latency_cache:
+        g.autosave_latency_cache(args.latency_cache)          # checkpoint after every searched block
     q_ios = g.schedule_dp(args.r, args.s)                      # device-measured stage costs (Alg. 1)
     if args.latency_cache and not os.path.exists(args.latency_cache):
         g.save_latency_cache(args.latency_cache)

@@ -190,6 +190,9 @@ IOS_API ios_status ios_stage_trace(ios_graph g, const int32_t* ops, int32_t n_op
 /* ---- stage-latency cache (checkpoint / resume of long searches) ------------------------------ */
 IOS_API ios_status ios_latency_cache_save(ios_graph g, const char* path);
 IOS_API ios_status ios_latency_cache_load(ios_graph g, const char* path);
+/* Checkpoint the cache to `path` after every block the device-profiled DP finishes measuring, so a
+ * long search (NASNet, RandWire) resumes with ios_latency_cache_load; NULL or "" turns it off. */
+IOS_API ios_status ios_latency_cache_autosave(ios_graph g, const char* path);
 
 IOS_API const char* ios_last_error(void);
 IOS_API void ios_schedule_destroy(ios_schedule q);

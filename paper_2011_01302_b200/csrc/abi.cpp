@@ -454,9 +454,11 @@ ios_status ios_schedule_launches(ios_graph gh, ios_schedule qh, int32_t* n) {
   ABI_END
 }
 
-// Latency cache file: one line per measured stage, "block_pos mask strategy ms" (text, versioned
-// by the graph signature line so a cache from another graph/math/batch is rejected).
-static std::string graph_signature(const Graph& g) {
+}  // extern "C"
+
+// Latency cache file: one line per measured stage, "block_signature mask strategy ms" (text,
+// versioned by the graph signature line so a cache from another graph/math/batch is rejected).
+std::string graph_signature(const Graph& g) {
   std::ostringstream s;
   s << "ios-latency-cache v2 batch=" << g.batch << " math=" << (int)g.math << " ops=" << g.ops.size();
   uint64_t h = 1469598103934665603ull;
@@ -469,15 +471,34 @@ static std::string graph_signature(const Graph& g) {
   return s.str();
 }
 
+namespace ios {
+void save_latency_cache(const Graph& g, const std::string& path) {
+  const std::string tmp = path + ".tmp";
+  {
+    std::ofstream f(tmp);
+    if (!f) IOS_FAIL(IOS_ERR_INVALID_ARG, "cannot write " + path);
+    f << graph_signature(g) << "\n";
+    f.precision(17);
+    for (auto& [k, v] : g.latency_cache)
+      f << std::get<0>(k) << " " << std::get<1>(k) << " " << std::get<2>(k) << " " << v << "\n";
+  }
+  std::rename(tmp.c_str(), path.c_str());
+}
+}  // namespace ios
+
+extern "C" {
+
 ios_status ios_latency_cache_save(ios_graph gh, const char* path) {
   ABI_BEGIN
   REQUIRE(gh && path, "bad arguments");
-  std::ofstream f(path);
-  if (!f) IOS_FAIL(IOS_ERR_INVALID_ARG, std::string("cannot write ") + path);
-  f << graph_signature(gh->g) << "\n";
-  f.precision(17);
-  for (auto& [k, v] : gh->g.latency_cache)
-    f << std::get<0>(k) << " " << std::get<1>(k) << " " << std::get<2>(k) << " " << v << "\n";
+  save_latency_cache(gh->g, path);
+  ABI_END
+}
+
+ios_status ios_latency_cache_autosave(ios_graph gh, const char* path) {
+  ABI_BEGIN
+  REQUIRE(gh, "bad arguments");
+  gh->g.cache_autosave = path ? path : "";
   ABI_END
 }
 

@@ -183,6 +183,7 @@ double schedule_dp(Graph& g, int r, int s, int set, ios_cost_fn cost, void* ctx,
       probe.run(&q0);
       measure_stages(g, bp, need);
       n_costed += (int64_t)need.size();
+      if (!need.empty() && !g.cache_autosave.empty()) save_latency_cache(g, g.cache_autosave);
     }
     BlockDP dp(g, bp, r, s, set, fn);
     std::vector<std::pair<uint64_t, int>> q;

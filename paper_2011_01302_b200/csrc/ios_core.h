@@ -65,6 +65,7 @@ struct Graph {
   // NASNet cells) share their measurements
   std::map<std::tuple<uint64_t, uint64_t, int>, double> latency_cache;
   std::vector<uint64_t> block_sigs;   // lazily computed
+  std::string cache_autosave;         // checkpoint the latency cache here after each block's search
   uint64_t block_sig(int bpos);
   DeviceState* dev = nullptr;
   ~Graph();
@@ -98,6 +99,7 @@ struct Schedule {
 };
 
 void validate_schedule(const Graph& g, const Schedule& q);   // throws BAD_SCHEDULE / NOT_MERGEABLE
+void save_latency_cache(const Graph& g, const std::string& path);
 
 // ------------------------------------------------------------------------------------ device
 double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const ios_profile_opts* opts);

@@ -79,6 +79,7 @@ def _load():
         "ios_schedule_launches": [P, P, pI32],
         "ios_latency_cache_save": [P, C.c_char_p],
         "ios_latency_cache_load": [P, C.c_char_p],
+        "ios_latency_cache_autosave": [P, C.c_char_p],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -307,3 +308,7 @@ class Graph:
 
     def load_latency_cache(self, path: str) -> None:
         _check(lib.ios_latency_cache_load(self.handle, path.encode()))
+
+    def autosave_latency_cache(self, path: str) -> None:
+        """Checkpoint the stage-latency cache after every searched block (resume long searches)."""
+        _check(lib.ios_latency_cache_autosave(self.handle, path.encode()))

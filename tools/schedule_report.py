@@ -15,6 +15,8 @@ net = W.build(a.net, math=NETS[a.net]["math"])
 g = Graph.from_netspec(net, NETS[a.net]["math"])
 if a.latency_cache and os.path.exists(a.latency_cache):
     g.load_latency_cache(a.latency_cache)
+if a.latency_cache:
+    g.autosave_latency_cache(a.latency_cache)
 q = g.schedule_dp(a.r, a.s)
 if a.latency_cache and not os.path.exists(a.latency_cache):
     g.save_latency_cache(a.latency_cache)
