@@ -138,7 +138,6 @@ ios_status ios_graph_create(int32_t batch, int32_t c, int32_t h, int32_t w, ios_
   ABI_BEGIN
   REQUIRE(out && batch > 0 && c > 0 && h > 0 && w > 0, "bad graph input shape");
   REQUIRE(math == IOS_MATH_TF32 || math == IOS_MATH_BF16 || math == IOS_MATH_FP32_SIMT, "bad math mode");
-  if (math == IOS_MATH_FP32_SIMT) IOS_FAIL(IOS_ERR_UNSUPPORTED, "IOS_MATH_FP32_SIMT is not implemented yet");
   auto* gh = new ios_graph_s();
   Graph& g = gh->g;
   g.batch = batch;

@@ -114,7 +114,9 @@ uint16_t bf16_rne_bits(float x) {
 // order: [k chunk][n / 8][8 pieces of 16 B][n % 8][16 B]. Any BN rows starting at a multiple of 8
 // of one chunk are then one contiguous run of BN * 128 bytes (one cp.async.bulk).
 template <class F>
-void* pack_gemm(DeviceState& d, int N, int K, bool bf16, F w, int* n8_out, std::vector<void*>* owner = nullptr) {
+void* pack_gemm(DeviceState& d, int N, int K, int dtype, F w, int* n8_out, std::vector<void*>* owner = nullptr) {
+  // dtype: ET_F32 -> TF32-rounded (RNE) fp32, ET_BF16 -> bf16 (RNE), ET_F32X -> exact fp32
+  const bool bf16 = dtype == ET_BF16;
   const int esz = bf16 ? 2 : 4, elems = kChunkBytes / esz, vec = 16 / esz;
   const int kch = (K + elems - 1) / elems;
   const int n8 = round_up(N, 8);
@@ -128,6 +130,8 @@ void* pack_gemm(DeviceState& d, int N, int K, bool bf16, F w, int* n8_out, std::
       if (bf16) {
         const uint16_t b = bf16_rne_bits(v);
         std::memcpy(&buf[off], &b, 2);
+      } else if (dtype == ET_F32X) {
+        std::memcpy(&buf[off], &v, 4);                 // exact fp32 (CUDA-core FMA path)
       } else {
         const uint32_t b = tf32_rne_bits(v);
         std::memcpy(&buf[off], &b, 4);
@@ -212,7 +216,7 @@ void ensure_device(Graph& g) {
     }
   }
   // ---- weights
-  const bool bf16 = g.math == IOS_MATH_BF16;
+  const int wdt = g.dtype();
   for (int v = 1; v < n; ++v) {
     const Op& o = g.ops[v];
     OpDev& e = d.od[v];
@@ -221,7 +225,7 @@ void ensure_device(Graph& g) {
     if (o.kind == IOS_OP_CONV || o.kind == IOS_OP_LINEAR) {
       const int cin = x.C, cin_p = x.Cp, kh = o.kh, kw = o.kw;
       const float* W = o.weight.data();
-      e.wpack = pack_gemm(d, o.Cp, kh * kw * cin_p, bf16, [&](int nn, int k) -> float {
+      e.wpack = pack_gemm(d, o.Cp, kh * kw * cin_p, wdt, [&](int nn, int k) -> float {
         if (nn >= o.cout) return 0.0f;
         const int tap = k / cin_p, ci = k % cin_p;
         if (ci >= cin) return 0.0f;
@@ -237,7 +241,7 @@ void ensure_device(Graph& g) {
         for (int t = 0; t < kk; ++t) dw[(size_t)ch * kk + t] = o.weight[(size_t)ch * kk + t];
       e.dw = upload(d, dw);
       const float* PW = o.weight.data() + (size_t)c * kk;
-      e.wpack = pack_gemm(d, o.Cp, cp, bf16, [&](int nn, int k) -> float {
+      e.wpack = pack_gemm(d, o.Cp, cp, wdt, [&](int nn, int k) -> float {
         return (nn < o.cout && k < c) ? PW[(size_t)nn * c + k] : 0.0f;
       }, &e.wpack_n8);
       std::vector<float> b(o.bias);
@@ -254,6 +258,7 @@ struct GemmSpec {
   int M, N16, K, kch, Npad8;
   int BN, ntn, mt, split, cps;
   int swap;   // swap-AB: weights are the 128-row MMA operand, the (<= 128) pixels are N
+  int max_bn = kMaxBN;
 };
 
 bool swap_enabled() {
@@ -297,10 +302,10 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       continue;
     }
     p->mt = (p->M + kBM - 1) / kBM;
-    if (p->N16 <= kMaxBN) {
+    if (p->N16 <= p->max_bn) {
       p->BN = p->N16;
     } else {
-      const int nt = (p->N16 + kMaxBN - 1) / kMaxBN;
+      const int nt = (p->N16 + p->max_bn - 1) / p->max_bn;
       p->BN = round_up((p->N16 + nt - 1) / nt, 16);
     }
     p->ntn = (p->N16 + p->BN - 1) / p->BN;
@@ -401,7 +406,8 @@ struct PlanBuilder {
     p.seg_begin = (int)segs.size();
     GemmSpec& s = specs[pi];
     s.Npad8 = n8;
-    s.swap = (p.M <= kBM && swap_enabled()) ? 1 : 0;
+    s.swap = (p.M <= kBM && swap_enabled() && g.math != IOS_MATH_FP32_SIMT) ? 1 : 0;
+    s.max_bn = g.math == IOS_MATH_FP32_SIMT ? 32 : kMaxBN;   // SIMT: 32 columns in registers
     s.M = p.M;
     s.N16 = round_up(Ntot, 16);
     s.K = p.K;
@@ -483,7 +489,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       }
       const int cin = x.C, cin_p = x.Cp;
       int merged_n8 = 0;
-      plan->merged_pack = pack_gemm(d, ntot, KH * KW * cin_p, g.math == IOS_MATH_BF16, [&](int nn, int k) -> float {
+      plan->merged_pack = pack_gemm(d, ntot, KH * KW * cin_p, g.dtype(), [&](int nn, int k) -> float {
         int bi = (int)ops.size() - 1;
         while (row0[bi] > nn) --bi;
         const Op& o = g.ops[ops[bi]];
@@ -600,7 +606,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       p.fd_cin = make_fastdiv((uint32_t)in.C);
       p.fd_kw = make_fastdiv((uint32_t)p.kw);
       // A via TMA when it is a plain [M, C] matrix: 1x1, stride 1, no padding, no pre-ReLU
-      p.a_tma = (p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 && p.pw == 0 &&
+      p.a_tma = (g.math != IOS_MATH_FP32_SIMT && p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 && p.pw == 0 &&
                  !(p.flags & IOS_F_RELU_PRE)) ? 1 : 0;
       p.swap_ab = s.swap;
       p.BN = s.BN;

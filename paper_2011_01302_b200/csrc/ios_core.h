@@ -70,7 +70,7 @@ struct Graph {
   DeviceState* dev = nullptr;
   ~Graph();
 
-  int dtype() const { return math == IOS_MATH_BF16 ? ET_BF16 : ET_F32; }
+  int dtype() const { return math == IOS_MATH_BF16 ? ET_BF16 : math == IOS_MATH_FP32_SIMT ? ET_F32X : ET_F32; }
   int esize() const { return math == IOS_MATH_BF16 ? 2 : 4; }
   // stage helpers
   uint64_t mask_of(const std::vector<int>& ops, int* bpos) const;   // throws NOT_A_STAGE

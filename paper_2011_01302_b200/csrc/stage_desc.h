@@ -37,7 +37,8 @@ enum ProblemKind : int32_t {
   PK_DWCONV = 6,    // sepconv front half: ReLU(sum_i w_i x_i) -> depthwise k x k
 };
 
-enum ElemType : int32_t { ET_F32 = 0, ET_BF16 = 1 };
+// ET_F32: fp32 storage rounded to TF32 (tcgen05 kind::tf32); ET_F32X: exact fp32, CUDA-core FMA GEMM
+enum ElemType : int32_t { ET_F32 = 0, ET_BF16 = 1, ET_F32X = 2 };
 
 // An NHWC activation view: element (n, h, w, c) at ptr + ((n*H + h)*W + w)*cstride + coff + c.
 // C is the padded channel count (multiple of 8); channels [Cl, C) hold zeros.

@@ -173,6 +173,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// accumulator access for the epilogue: TMEM (tcgen05 paths) or the CUDA-core FP32 registers (ET_F32X)
+template <int DT>
+__device__ __forceinline__ void acc_ld16(uint32_t taddr, const float* sacc, int c0, uint32_t* v) {
+  if constexpr (DT == ET_F32X) {
+    if (c0 == 0) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(sacc[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(sacc[16 + e]);
+    }
+  } else {
+    tmem_ld16(taddr, v);
+  }
+}
+template <int DT>
+__device__ __forceinline__ void acc_wait() {
+  if constexpr (DT != ET_F32X) tmem_ld_wait();
+}
 
 __device__ __forceinline__ float tf32_round(float x) {
   uint32_t r;
@@ -186,9 +205,12 @@ struct Vec8 {
   float v[8];
 };
 
+// storage rounding: TF32 mode keeps activations TF32-representable (Z14); FP32-SIMT stores exact fp32
+__device__ __forceinline__ float rnd(float x, int dtype) { return dtype == ET_F32 ? tf32_round(x) : x; }
+
 __device__ __forceinline__ void load_vec(const View& vw, int dtype, int64_t pix, int c, float* out, int nv) {
   // nv = elements per 16 B (4 fp32 / 8 bf16); cache-global loads (other CTAs wrote these in this launch)
-  if (dtype == ET_F32) {
+  if (dtype != ET_BF16) {
     const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(vw.ptr) + pix * vw.cstride + vw.coff + c);
     float4 a = __ldcg(p);
     out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
@@ -206,8 +228,8 @@ __device__ __forceinline__ void load_vec(const View& vw, int dtype, int64_t pix,
 }
 
 __device__ __forceinline__ void store_vec(const View& vw, int dtype, int64_t pix, int c, const float* in) {
-  if (dtype == ET_F32) {
-    float4 a = make_float4(tf32_round(in[0]), tf32_round(in[1]), tf32_round(in[2]), tf32_round(in[3]));
+  if (dtype != ET_BF16) {
+    float4 a = make_float4(rnd(in[0], dtype), rnd(in[1], dtype), rnd(in[2], dtype), rnd(in[3], dtype));
     *reinterpret_cast<float4*>(reinterpret_cast<float*>(vw.ptr) + pix * vw.cstride + vw.coff + c) = a;
   } else {
     uint4 a;
@@ -219,14 +241,14 @@ __device__ __forceinline__ void store_vec(const View& vw, int dtype, int64_t pix
 }
 
 __device__ __forceinline__ float load_elem(const View& vw, int dtype, int64_t pix, int c) {
-  if (dtype == ET_F32) return __ldcg(reinterpret_cast<const float*>(vw.ptr) + pix * vw.cstride + vw.coff + c);
+  if (dtype != ET_BF16) return __ldcg(reinterpret_cast<const float*>(vw.ptr) + pix * vw.cstride + vw.coff + c);
   const unsigned short* p = reinterpret_cast<const unsigned short*>(vw.ptr) + pix * vw.cstride + vw.coff + c;
   unsigned short u = __ldcg(p);
   return __uint_as_float(((uint32_t)u) << 16);
 }
 __device__ __forceinline__ void store_elem(const View& vw, int dtype, int64_t pix, int c, float x) {
-  if (dtype == ET_F32)
-    reinterpret_cast<float*>(vw.ptr)[pix * vw.cstride + vw.coff + c] = tf32_round(x);
+  if (dtype != ET_BF16)
+    reinterpret_cast<float*>(vw.ptr)[pix * vw.cstride + vw.coff + c] = rnd(x, dtype);
   else
     reinterpret_cast<__nv_bfloat16*>(vw.ptr)[pix * vw.cstride + vw.coff + c] = __float2bfloat16_rn(x);
 }
@@ -488,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kMmaWarp && sd.has_gemm) {
+  if (warp == kMmaWarp && sd.has_gemm && DT != ET_F32X) {
     __syncwarp();
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(kTmemCols)
@@ -702,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     // ============================================================== MMA ISSUER
     // The whole warp walks the tiles and waits on the barriers (warp-uniform control flow); one
     // elected lane issues tcgen05.mma / tcgen05.commit.
-    if (sd.has_gemm) {
+    if (sd.has_gemm && DT != ET_F32X) {
       Ring ring;
       int acc = 0;
       uint32_t acc_phase = 0;
@@ -748,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   } else {
     // ============================================================== EPILOGUE + SIMT (warps 4-7)
     const int etid = tid - kEpilogueWarp0 * 32;   // 0..127 == TMEM lane == tile row
+    Ring ering;                                   // FP32-SIMT mode: the epilogue consumes the smem ring
     const int lane_base = (warp & 3) * 32;        // TMEM lanes this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -809,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               if (DT == ET_BF16)
                 *reinterpret_cast<__nv_bfloat16*>(ocol + px * ostride) = __float2bfloat16_rn(o);
               else
-                *reinterpret_cast<float*>(ocol + px * ostride) = tf32_round(o);
+                *reinterpret_cast<float*>(ocol + px * ostride) = rnd(o, DT);
             }
           }
           tc_fence_before();
@@ -858,7 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               if (DT == ET_BF16)
                 *reinterpret_cast<__nv_bfloat16*>(ocol + px * ostride) = __float2bfloat16_rn(o);
               else
-                *reinterpret_cast<float*>(ocol + px * ostride) = tf32_round(o);
+                *reinterpret_cast<float*>(ocol + px * ostride) = rnd(o, DT);
             }
           }
         }
@@ -871,12 +894,51 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         if (acc == 0) acc_phase ^= 1u;
         continue;
       }
+      // FP32-SIMT mode: the epilogue warps are the GEMM consumer: thread = tile row, BN <= 32
+      // columns in registers, exact fp32 FMA over every K chunk the producers stage
+      float sacc[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) sacc[e] = 0.f;
+      if constexpr (DT == ET_F32X) {
+        const int c0 = s * P.chunks_per_split;
+        const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
+        const int bn = P.BN;
+        for (int c = c0; c < c1; ++c) {
+          mbar_wait(smem_u32(&full[ering.slot]), ering.phase);
+          const uint8_t* As = sA + ering.slot * kAStageBytes + (etid >> 3) * 1024 + (etid & 7) * 16;
+          const uint8_t* Bs = sB + ering.slot * kBStageBytes;
+          float a[32];
+#pragma unroll
+          for (int pc = 0; pc < 8; ++pc) {
+            const float4 v = *reinterpret_cast<const float4*>(As + pc * 128);
+            a[4 * pc] = v.x; a[4 * pc + 1] = v.y; a[4 * pc + 2] = v.z; a[4 * pc + 3] = v.w;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j >= bn) break;
+            const uint8_t* brow = Bs + (j >> 3) * 1024 + (j & 7) * 16;
+            float accj = sacc[j];
+#pragma unroll
+            for (int pc = 0; pc < 8; ++pc) {
+              const float4 b = *reinterpret_cast<const float4*>(brow + pc * 128);   // broadcast
+              accj = fmaf(a[4 * pc], b.x, accj);
+              accj = fmaf(a[4 * pc + 1], b.y, accj);
+              accj = fmaf(a[4 * pc + 2], b.z, accj);
+              accj = fmaf(a[4 * pc + 3], b.w, accj);
+            }
+            sacc[j] = accj;
+          }
+          named_bar(2, 128);
+          if (etid == 0) mbar_arrive(smem_u32(&empty[ering.slot]));   // slot free for the producers
+          ering.next();
+        }
+      }
       // stage this tile's bias slice in smem while the MMAs run (one load round trip, off the
       // critical path); the previous tile's readers of this buffer are past the barrier below
       float* sbias = sbias_all + acc * kMaxBN;
       for (int i = etid; i < P.BN; i += 128) sbias[i] = __ldg(bias + nt * P.BN + i);
       named_bar(2, 128);
-      mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+      if (DT != ET_F32X) mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       if (etid == 0 && tfirst) IOS_TRACE(5);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
@@ -898,9 +960,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
         for (int c0 = 0; c0 < P.BN; c0 += 32) {
           uint32_t va[16], vb[16];
-          tmem_ld16(tbase + c0, va);
-          tmem_ld16(tbase + c0 + 16, vb);
-          tmem_ld_wait();
+          acc_ld16<DT>(tbase + c0, sacc, c0, va);
+          acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
+          acc_wait<DT>();
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(13);
           float o[32];
 #pragma unroll
@@ -919,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               }
             } else {
 #pragma unroll
-              for (int q = 0; q < 4; ++q) w[q] = __float_as_uint(tf32_round(o[p * 4 + q]));
+              for (int q = 0; q < 4; ++q) w[q] = __float_as_uint(rnd(o[p * 4 + q], DT));
             }
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * (PPR * 16) + ((p ^ (lane & 7)) % PPR) * 16),
                          "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
@@ -943,12 +1005,12 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(15);
         }
         tc_fence_before();
-        mbar_arrive(smem_u32(&tempty[acc]));
+        if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
       } else if (P.split == 1) {
         for (int c0 = 0; c0 < P.BN; c0 += 16) {
           uint32_t v[16];
-          tmem_ld16(tbase + c0, v);
-          tmem_ld_wait();
+          acc_ld16<DT>(tbase + c0, sacc, c0, v);
+          acc_wait<DT>();
           if (!valid) continue;
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
@@ -973,7 +1035,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           }
         }
         tc_fence_before();
-        mbar_arrive(smem_u32(&tempty[acc]));
+        if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
       } else {
         // split-K: every split adds its fp32 partial into the tile's zeroed accumulator with
         // vector reductions (fire-and-forget at L2); the last arriving split reads the sum once,
@@ -984,9 +1046,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const int wr0 = (warp & 3) * 32;
         for (int c0 = 0; c0 < P.BN; c0 += 32) {
           uint32_t va[16], vb[16];
-          tmem_ld16(tbase + c0, va);
-          tmem_ld16(tbase + c0 + 16, vb);
-          tmem_ld_wait();
+          acc_ld16<DT>(tbase + c0, sacc, c0, va);
+          acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
+          acc_wait<DT>();
           // stage (swizzled) then coalesced vector reductions: 4 rows x 128 B per instruction
 #pragma unroll
           for (int p = 0; p < 8; ++p) {
@@ -1009,7 +1071,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           __syncwarp();
         }
         tc_fence_before();
-        mbar_arrive(smem_u32(&tempty[acc]));
+        if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
         named_bar(2, 128);
         if (etid == 0) {
           const int old = atom_acqrel_add(counters + P.tilectr_idx + out_tile, 1);
@@ -1064,7 +1126,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               } else {
                 *reinterpret_cast<float4*>(reinterpret_cast<float*>(sgp->out.ptr) + pix * sgp->out.cstride +
                                            sgp->out.coff + ncol - sgp->n0) =
-                    make_float4(tf32_round(o[0]), tf32_round(o[1]), tf32_round(o[2]), tf32_round(o[3]));
+                    make_float4(rnd(o[0], DT), rnd(o[1], DT), rnd(o[2], DT), rnd(o[3], DT));
               }
             }
           }
@@ -1091,7 +1153,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   __syncwarp();   // the MMA warp ran its loop on lane 0 only
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp && sd.has_gemm) {
+  if (warp == kMmaWarp && sd.has_gemm && DT != ET_F32X) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols) : "memory");
   }
@@ -1150,6 +1212,8 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
     cudaError_t e = cudaFuncSetAttribute(ios_stage_kernel<ET_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(ios_stage_kernel<ET_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ios_stage_kernel<ET_F32X>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -1164,6 +1228,7 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (dtype == ET_BF16) return cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_BF16>, sd);
+  if (dtype == ET_F32X) return cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32X>, sd);
   return cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32>, sd);
 }
 

@@ -104,3 +104,16 @@ def test_network_sequential_and_greedy(torch_cuda, name, math):
     assert rel_err(y, ref) < TOL[math]
     _, _, y2 = _run(net, math, "greedy", torch_cuda)
     assert rel_err(y2, ref) < TOL[math]
+
+
+@pytest.mark.parametrize("name", ["fig2", "tiny_mixed"])
+def test_fp32_simt_mode_1e5(torch_cuda, name):
+    """IOS_MATH_FP32_SIMT: exact fp32 storage, CUDA-core FMA GEMM; north star tolerance 1e-5."""
+    net = W.build(name)
+    g, q, y = _run(net, "fp32_simt", "sequential", torch_cuda)
+    errs = per_op_errors(net, g, "fp32_simt")
+    assert max(errs.values()) < 1e-5, errs
+    ref = OracleGraph(net).run_sequential(net.make_input())[net.n_ops]
+    assert rel_err(y, ref) < 1e-5
+    _, _, y2 = _run(net, "fp32_simt", "greedy", torch_cuda)
+    assert rel_err(y2, ref) < 1e-5
