@@ -29,9 +29,10 @@ struct OpDev {
   void* wpack = nullptr;      // packed GEMM weights (conv / linear / sepconv pointwise)
   int wpack_n8 = 0;           // packed rows (multiple of 8)
   float* bias = nullptr;      // fp32, zero padded
-  float* dw = nullptr;        // sepconv depthwise weights fp32 [Cp_in][kh*kw]
+  float* dw = nullptr;        // sepconv depthwise weights fp32, tap-major [kh*kw][Cp_in]
   float* add_w = nullptr;     // add / sepconv aggregation weights
   View dw_out{};              // sepconv depthwise scratch (NHWC, Cp_in channels)
+  int tt = 0, kblk = 0;       // weights packed for the tap-TMA im2col path (K = taps x kblk blocks)
 };
 
 }  // namespace
@@ -144,6 +145,53 @@ void* pack_gemm(DeviceState& d, int N, int K, int dtype, F w, int* n8_out, std::
 
 int64_t view_elems(const Op& o, int C) { return (int64_t)o.N * o.H * o.W * C; }
 
+// Output patch of one tap-TMA M tile: tN images x tR rows x tWt columns (<= 128 pixels, TMA box
+// dims <= 256 input elements). Whole images when everything fits one tile (the swap-AB case: the
+// tile row is then the pixel index); otherwise the (tWt, tR) with the fewest tiles.
+struct TTGeom {
+  int tN = 0, tR = 0, tWt = 0, tiles_h = 0, tiles_w = 0, tiles = 0;
+};
+TTGeom tt_geometry(int batch, int Ho, int Wo, int sh, int sw) {
+  TTGeom best;
+  if ((int64_t)batch * Ho * Wo <= kBM && Wo * sw <= 256 && Ho * sh <= 256) {
+    best.tN = batch; best.tR = Ho; best.tWt = Wo;
+    best.tiles_h = best.tiles_w = best.tiles = 1;
+    return best;
+  }
+  for (int wt = std::min(Wo, kBM); wt >= 1; --wt) {
+    if (wt * sw > 256) continue;
+    const int r = std::min(std::min(Ho, kBM / wt), 256 / sh);
+    if (r < 1) continue;
+    const int tn = (r == Ho && wt == Wo) ? std::max(1, std::min(batch, kBM / (Ho * Wo))) : 1;
+    const int th = (Ho + r - 1) / r, tw = (Wo + wt - 1) / wt;
+    const int tiles = ((batch + tn - 1) / tn) * th * tw;
+    if (best.tiles == 0 || tiles < best.tiles) {
+      best.tN = tn; best.tR = r; best.tWt = wt;
+      best.tiles_h = th; best.tiles_w = tw; best.tiles = tiles;
+    }
+  }
+  return best;
+}
+
+// Tap-TMA im2col eligibility: returns the number of 128 B channel blocks per tap (0 = use the
+// cp.async gather or the 2D TMA path). Pre-ReLU convs need the gather (the ReLU is applied on the
+// way to smem); 1x1/s1/unpadded convs take the plain 2D TMA; narrow inputs would pad K too much;
+// patch tiles must not waste much more M than the gather's dense 128-pixel tiles.
+bool tap_tma_enabled();
+int tap_tma_blocks(const Graph& g, int cin_p, int kh, int kw, int sh, int sw, int ph, int pw, int flags, int batch,
+                   int Ho, int Wo) {
+  if (g.math == IOS_MATH_FP32_SIMT || (flags & IOS_F_RELU_PRE)) return 0;
+  if (!tap_tma_enabled()) return 0;
+  if (kh == 1 && kw == 1 && sh == 1 && sw == 1 && ph == 0 && pw == 0) return 0;
+  if (sh > 8 || sw > 8) return 0;
+  const int elems = kChunkBytes / g.esize();
+  const int kblk = (cin_p + elems - 1) / elems;
+  if (cin_p < 16 || kblk * elems * 2 > cin_p * 3) return 0;   // at most 1.5x K padding
+  const int64_t dense = ((int64_t)batch * Ho * Wo + kBM - 1) / kBM;
+  if ((int64_t)tt_geometry(batch, Ho, Wo, sh, sw).tiles * 4 > dense * 5) return 0;
+  return kblk;
+}
+
 void ensure_device(Graph& g) {
   if (g.dev && g.dev->ready) return;
   if (!g.dev) g.dev = new DeviceState();
@@ -225,9 +273,14 @@ void ensure_device(Graph& g) {
     if (o.kind == IOS_OP_CONV || o.kind == IOS_OP_LINEAR) {
       const int cin = x.C, cin_p = x.Cp, kh = o.kh, kw = o.kw;
       const float* W = o.weight.data();
-      e.wpack = pack_gemm(d, o.Cp, kh * kw * cin_p, wdt, [&](int nn, int k) -> float {
+      // tap-TMA im2col packs K per tap in whole 128 B channel blocks (zero rows for the padding)
+      e.kblk = o.kind == IOS_OP_CONV ? tap_tma_blocks(g, cin_p, kh, kw, o.sh, o.sw, o.ph, o.pw, o.flags, g.batch, o.H, o.W)
+                                     : 0;
+      e.tt = e.kblk > 0;
+      const int tapk = e.tt ? e.kblk * (kChunkBytes / g.esize()) : cin_p;
+      e.wpack = pack_gemm(d, o.Cp, kh * kw * tapk, wdt, [&](int nn, int k) -> float {
         if (nn >= o.cout) return 0.0f;
-        const int tap = k / cin_p, ci = k % cin_p;
+        const int tap = k / tapk, ci = k % tapk;
         if (ci >= cin) return 0.0f;
         const int i = tap / kw, j = tap % kw;
         return W[(((size_t)nn * cin + ci) * kh + i) * kw + j];
@@ -236,9 +289,10 @@ void ensure_device(Graph& g) {
       e.bias = upload(d, b, (size_t)round_up(o.Cp, 256) + 16);
     } else if (o.kind == IOS_OP_SEPCONV) {
       const int c = x.C, cp = x.Cp, kk = o.kh * o.kw;
+      // tap-major [kh*kw][Cp]: a 16 B vector of consecutive channels per tap
       std::vector<float> dw((size_t)cp * kk, 0.0f);
       for (int ch = 0; ch < c; ++ch)
-        for (int t = 0; t < kk; ++t) dw[(size_t)ch * kk + t] = o.weight[(size_t)ch * kk + t];
+        for (int t = 0; t < kk; ++t) dw[(size_t)t * cp + ch] = o.weight[(size_t)ch * kk + t];
       e.dw = upload(d, dw);
       const float* PW = o.weight.data() + (size_t)c * kk;
       e.wpack = pack_gemm(d, o.Cp, cp, wdt, [&](int nn, int k) -> float {
@@ -259,7 +313,16 @@ struct GemmSpec {
   int BN, ntn, mt, split, cps;
   int swap;   // swap-AB: weights are the 128-row MMA operand, the (<= 128) pixels are N
   int max_bn = kMaxBN;
+  int tt_tiles = 0;   // tap-TMA: number of patch M tiles (0 = dense 128-pixel tiles)
 };
+
+bool tap_tma_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("IOS_TAP_TMA");
+    return v ? atoi(v) != 0 : true;
+  }();
+  return on;
+}
 
 bool swap_enabled() {
   static const bool on = [] {
@@ -275,6 +338,7 @@ struct TileKnobs {
   int min_cps;        // never split K below this many 128 B chunks per unit
   int min_bn_small;   // narrowest N tile for small-M (<= 2 m-tiles) GEMMs
   int min_bn;         // narrowest N tile otherwise
+  int one_wave;       // never refine past the target unit count (one wave of CTAs)
 };
 static TileKnobs tile_knobs() {
   static TileKnobs k = [] {
@@ -283,7 +347,7 @@ static TileKnobs tile_knobs() {
       return v ? atoi(v) : d;
     };
     return TileKnobs{env("IOS_TARGET_UNITS", 0), env("IOS_MIN_CPS", 4), env("IOS_MIN_BN_SMALL", 16),
-                     env("IOS_MIN_BN", 32)};
+                     env("IOS_MIN_BN", 32), env("IOS_ONE_WAVE", 1)};
   }();
   return k;
 }
@@ -301,7 +365,7 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       p->cps = p->kch;
       continue;
     }
-    p->mt = (p->M + kBM - 1) / kBM;
+    p->mt = p->tt_tiles ? p->tt_tiles : (p->M + kBM - 1) / kBM;
     if (p->N16 <= p->max_bn) {
       p->BN = p->N16;
     } else {
@@ -333,11 +397,19 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       }
     }
     if (!best) break;
-    if (!best->swap && best->BN >= 2 * (best->mt <= 2 ? kn.min_bn_small : kn.min_bn)) {
+    // never refine past one wave: a step that would push the unit count over the target is
+    // replaced by the largest split-K that still fits, or refinement stops
+    const int cur = best->mt * best->ntn * best->split;
+    const int others = units - cur;
+    const bool can_n = !best->swap && best->BN >= 2 * (best->mt <= 2 ? kn.min_bn_small : kn.min_bn);
+    if (can_n && (!kn.one_wave || others + 2 * cur <= target)) {
       best->BN = round_up(best->BN / 2, 16);
       best->ntn = (best->N16 + best->BN - 1) / best->BN;
     } else {
-      const int want = best->split * 2;
+      int want = best->split * 2;
+      const int room = (target - others) / (best->mt * best->ntn);
+      if (kn.one_wave && want > room) want = room;
+      if (want <= best->split || (best->kch + want - 1) / want < kn.min_cps) break;
       best->cps = (best->kch + want - 1) / want;
       best->split = (best->kch + best->cps - 1) / best->cps;
     }
@@ -385,7 +457,7 @@ struct PlanBuilder {
     }
   }
   int gemm(int in_op_view_src, const View& in, void* wpack, int n8, float* bias, int Ntot, int kh, int kw, int sh,
-           int sw, int ph, int pw, int Ho, int Wo, int flags) {
+           int sw, int ph, int pw, int Ho, int Wo, int flags, int kblk = 0) {
     (void)in_op_view_src;
     const int pi = add_problem(PK_GEMM);
     Problem& p = probs[pi];
@@ -400,13 +472,22 @@ struct PlanBuilder {
     p.Npad8 = n8;
     p.bias = (uint64_t)bias;
     p.M = g.batch * Ho * Wo;
-    p.K = kh * kw * in.C;
     const int elems = kChunkBytes / g.esize();
+    p.K = kblk ? kh * kw * kblk * elems : kh * kw * in.C;
     p.k_chunks = (p.K + elems - 1) / elems;
     p.seg_begin = (int)segs.size();
     GemmSpec& s = specs[pi];
     s.Npad8 = n8;
     s.swap = (p.M <= kBM && swap_enabled() && g.math != IOS_MATH_FP32_SIMT) ? 1 : 0;
+    if (kblk) {
+      const TTGeom tg = tt_geometry(g.batch, Ho, Wo, sh, sw);
+      p.tt = 1;
+      p.kblk = kblk;
+      p.tN = tg.tN; p.tR = tg.tR; p.tWt = tg.tWt;
+      p.tiles_h = tg.tiles_h; p.tiles_w = tg.tiles_w;
+      s.tt_tiles = tg.tiles;
+      if (tg.tiles != 1) s.swap = 0;   // swap-AB needs the whole image as one dense pixel tile
+    }
     s.max_bn = g.math == IOS_MATH_FP32_SIMT ? 32 : kMaxBN;   // SIMT: 32 columns in registers
     s.M = p.M;
     s.N16 = round_up(Ntot, 16);
@@ -488,14 +569,16 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
         ntot += g.ops[v].Cp;
       }
       const int cin = x.C, cin_p = x.Cp;
+      const int kblk = tap_tma_blocks(g, cin_p, KH, KW, f.sh, f.sw, PH, PW, f.flags, g.batch, f.H, f.W);
+      const int tapk = kblk ? kblk * (kChunkBytes / g.esize()) : cin_p;
       int merged_n8 = 0;
-      plan->merged_pack = pack_gemm(d, ntot, KH * KW * cin_p, g.dtype(), [&](int nn, int k) -> float {
+      plan->merged_pack = pack_gemm(d, ntot, KH * KW * tapk, g.dtype(), [&](int nn, int k) -> float {
         int bi = (int)ops.size() - 1;
         while (row0[bi] > nn) --bi;
         const Op& o = g.ops[ops[bi]];
         const int r = nn - row0[bi];
         if (r >= o.cout) return 0.0f;
-        const int tap = k / cin_p, ci = k % cin_p;
+        const int tap = k / tapk, ci = k % tapk;
         if (ci >= cin) return 0.0f;
         const int i = tap / KW - (-o.ph - st_h), j = tap % KW - (-o.pw - st_w);
         if (i < 0 || i >= o.kh || j < 0 || j >= o.kw) return 0.0f;
@@ -508,7 +591,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       }
       plan->merged_bias = upload(d, bias, 0, &plan->allocs);
       const int pi = b.gemm(f.inputs[0], d.od[f.inputs[0]].out, plan->merged_pack, merged_n8, plan->merged_bias,
-                            ntot, KH, KW, f.sh, f.sw, PH, PW, f.H, f.W, f.flags & IOS_F_RELU_PRE);
+                            ntot, KH, KW, f.sh, f.sw, PH, PW, f.H, f.W, f.flags & IOS_F_RELU_PRE, kblk);
       for (size_t bi = 0; bi < ops.size(); ++bi) {
         const Op& o = g.ops[ops[bi]];
         b.seg(pi, row0[bi], row0[bi] + o.Cp, d.od[ops[bi]].out, (o.flags & IOS_F_RELU_POST) ? 1 : 0);
@@ -526,7 +609,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
           case IOS_OP_LINEAR: {
             const int u = o.inputs[0];
             const int pi = b.gemm(u, d.od[u].out, e.wpack, e.wpack_n8, e.bias, o.Cp, o.kh, o.kw, o.sh, o.sw, o.ph, o.pw,
-                                  o.H, o.W, o.flags & IOS_F_RELU_PRE);
+                                  o.H, o.W, o.flags & IOS_F_RELU_PRE, e.kblk);
             b.seg(pi, 0, o.Cp, e.out, (o.flags & IOS_F_RELU_POST) ? 1 : 0);
             b.add_deps(pi, deps);
             b.op_probs[v] = {pi};
@@ -577,9 +660,18 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       Problem& p = b.probs[i];
       if (p.kind == PK_GEMM) continue;
       const int nvec = p.out.C / nv;
+      const bool sq = p.kh == p.kw && p.sh == p.sw && (p.sh == 1 || p.sh == 2);
+      const bool win = sq && ((p.kind == PK_DWCONV && (p.kh == 3 || p.kh == 5 || p.kh == 7) && p.n_in <= 8) ||
+                              ((p.kind == PK_MAXPOOL || p.kind == PK_AVGPOOL) && p.kh == 3));
       if (p.kind == PK_GAVGPOOL) {
         p.n_items = p.batch * nvec;
-        p.items_per_tile = 32;
+        p.items_per_tile = 16;
+      } else if (win) {
+        // quads of horizontally adjacent outputs (win_tile in stage_kernel.cu); one quad x vector
+        // per thread of a 128-thread tile
+        p.dwq = g.esize() == 2 ? 2 : 4;
+        p.n_items = p.batch * p.Ho * ((p.Wo + p.dwq - 1) / p.dwq);
+        p.items_per_tile = std::max(1, 128 / std::max(1, nvec));
       } else {
         // about 4 vector items per epilogue thread so the stage spreads over many SMs
         p.n_items = p.batch * p.Ho * p.Wo;
@@ -605,6 +697,13 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       p.fd_ntn = make_fastdiv((uint32_t)s.ntn);
       p.fd_cin = make_fastdiv((uint32_t)in.C);
       p.fd_kw = make_fastdiv((uint32_t)p.kw);
+      if (p.tt) {
+        p.fd_kblk = make_fastdiv((uint32_t)p.kblk);
+        p.fd_thw = make_fastdiv((uint32_t)(p.tR * p.tWt));
+        p.fd_tw = make_fastdiv((uint32_t)p.tWt);
+        p.fd_tilw = make_fastdiv((uint32_t)p.tiles_w);
+        p.fd_tilh = make_fastdiv((uint32_t)p.tiles_h);
+      }
       // A via TMA when it is a plain [M, C] matrix: 1x1, stride 1, no padding, no pre-ReLU
       p.a_tma = (g.math != IOS_MATH_FP32_SIMT && p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 && p.pw == 0 &&
                  !(p.flags & IOS_F_RELU_PRE)) ? 1 : 0;
@@ -636,7 +735,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       p.done_idx = 1 + i;
       for (int k = 0; k < p.n_deps; ++k) {
         const Problem& q = b.probs[p.dep_idx[k]];
-        p.dep_target[k] = q.kind == PK_GEMM ? q.m_tiles * q.n_tiles_n : q.n_tiles;
+        p.dep_target[k] = q.n_tiles;   // every unit (incl. each split-K part) signals once
         p.dep_idx[k] = 1 + p.dep_idx[k];
       }
       if (p.kind == PK_GEMM && p.split > 1) p.tilectr_idx += 1 + np;
@@ -657,20 +756,37 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       if (sb) std::memcpy(blob.data() + pb + vb, b.segs.data(), sb);
       // tensor maps for TMA-loaded A operands (global memory, 64 B aligned, written before launch)
       std::vector<CUtensorMap> maps;
+      const CUtensorMapDataType tdt =
+          g.math == IOS_MATH_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+      const cuuint32_t elems = (cuuint32_t)(kChunkBytes / g.esize());
       for (Problem& p : b.probs) {
-        if (p.kind != PK_GEMM || !p.a_tma) continue;
+        if (p.kind != PK_GEMM || !(p.a_tma || p.tt)) continue;
         const View& in = b.views[p.in_begin];
         CUtensorMap tm;
-        const cuuint64_t dims[2] = {(cuuint64_t)in.C, (cuuint64_t)p.M};
-        const cuuint64_t strides[1] = {(cuuint64_t)in.cstride * g.esize()};
-        const cuuint32_t box[2] = {(cuuint32_t)(kChunkBytes / g.esize()), (cuuint32_t)kBM};
-        const cuuint32_t estr[2] = {1, 1};
         void* base = reinterpret_cast<char*>(in.ptr) + (size_t)in.coff * g.esize();
-        CUresult r = encode_tiled()(&tm, g.math == IOS_MATH_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                            2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        CUresult r;
+        if (p.a_tma) {
+          // [M, C] matrix: 128 rows x 128 B per box
+          const cuuint64_t dims[2] = {(cuuint64_t)in.C, (cuuint64_t)p.M};
+          const cuuint64_t strides[1] = {(cuuint64_t)in.cstride * g.esize()};
+          const cuuint32_t box[2] = {elems, (cuuint32_t)kBM};
+          const cuuint32_t estr[2] = {1, 1};
+          r = encode_tiled()(&tm, tdt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        } else {
+          // NHWC input as a 4D tensor {C, W, H, N}; one box = tN x tR x tWt output pixels of one tap
+          // (element strides = conv strides) x one 128 B channel block; padding = out-of-bounds zeros
+          const cuuint64_t dims[4] = {(cuuint64_t)in.C, (cuuint64_t)in.W, (cuuint64_t)in.H, (cuuint64_t)p.batch};
+          const cuuint64_t rs = (cuuint64_t)in.cstride * g.esize();
+          const cuuint64_t strides[3] = {rs, rs * in.W, rs * in.W * in.H};
+          const cuuint32_t box[4] = {elems, (cuuint32_t)(p.tWt * p.sw), (cuuint32_t)(p.tR * p.sh), (cuuint32_t)p.tN};
+          const cuuint32_t estr[4] = {1, (cuuint32_t)p.sw, (cuuint32_t)p.sh, 1};
+          r = encode_tiled()(&tm, tdt, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (r != CUDA_SUCCESS) IOS_FAIL(IOS_ERR_CUDA, "tap-TMA tensor map rejected by the driver");
+        }
         if (r != CUDA_SUCCESS) {
           p.a_tma = 0;   // fall back to the cp.async gather
           continue;
@@ -681,7 +797,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       if (!maps.empty()) {
         void* mp = upload(d, maps, 0, &plan->allocs);
         for (Problem& p : b.probs)
-          if (p.kind == PK_GEMM && p.a_tma) p.tmap_a = (uint64_t)mp + p.tmap_a * sizeof(CUtensorMap);
+          if (p.kind == PK_GEMM && (p.a_tma || p.tt)) p.tmap_a = (uint64_t)mp + p.tmap_a * sizeof(CUtensorMap);
       }
       std::memcpy(blob.data(), b.probs.data(), pb);
       plan->dmem = upload(d, blob, 0, &plan->allocs);

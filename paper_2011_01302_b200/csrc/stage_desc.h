@@ -91,11 +91,19 @@ struct Problem {
   FastDiv fd_howo, fd_wo, fd_split, fd_ntn, fd_cin, fd_kw;   // divisors of the tile / im2col decode
   // SIMT geometry
   int32_t items_per_tile, n_items;  // items = output pixels (x channel vectors handled inside)
+  int32_t dwq;                      // window ops (dw / max / avg, square k in {3,5,7}, stride 1-2):
+                                    // items are quads of dwq horizontally adjacent output pixels
+                                    // sharing one loaded input row span (0 = one pixel per item)
   int32_t a_tma;                    // 1: the activation operand is a plain [M, C] matrix loaded by TMA
   int32_t swap_ab;                  // 1: weights are the MMA A operand (128 output channels per tile),
                                     //    the M (<= 128) pixels are MMA N = BN; m_tiles count channel tiles
-  int32_t pad2_;
-  uint64_t tmap_a;                  // global address of its CUtensorMap (2D tiled, 128B swizzle)
+  int32_t tt;                       // 1: "tap TMA" im2col: per K chunk (tap, 32/64-channel block) one 4D
+                                    //    tensor TMA of a (tN images x tR rows x tWt cols) output patch;
+                                    //    M tiles are such patches (tile row r = (nn*tR + i)*tWt + j);
+                                    //    K = taps x kblk channel blocks (zero-padded)
+  int32_t kblk, tN, tR, tWt, tiles_h, tiles_w;
+  FastDiv fd_kblk, fd_thw, fd_tw, fd_tilw, fd_tilh;
+  uint64_t tmap_a;                  // global address of its CUtensorMap (2D / 4D tiled, 128B swizzle)
 };
 
 struct StageDesc {

@@ -60,6 +60,13 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, uint64_t tmap, int c0,
       "l"(tmap), "r"(c0), "r"(c1), "r"(mbar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, uint64_t tmap, int c0, int c1, int c2, int c3,
+                                            uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cnt(uint32_t a, uint32_t n) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(n) : "memory");
 }
@@ -199,6 +206,27 @@ __device__ __forceinline__ float tf32_round(float x) {
   return __uint_as_float(r);
 }
 
+// Global stores as asm without a "memory" clobber: the descriptor table is read through generic
+// pointers, so a plain C++ store (or __stcg) makes the compiler re-load every descriptor field it
+// needs after each store, and a generic load behind a generic store waits for that store -- one
+// memory round trip per store. These stores cannot alias the descriptors; ordering against the
+// completion signals (asm volatile with "memory") is kept because volatile asm is never reordered.
+__device__ __forceinline__ void stg_f32(void* p, float v) { asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v)); }
+__device__ __forceinline__ void stg_b16(void* p, unsigned short v) { asm volatile("st.global.b16 [%0], %1;" ::"l"(p), "h"(v)); }
+__device__ __forceinline__ void stg_v2(void* p, uint32_t a, uint32_t b) {
+  asm volatile("st.global.v2.b32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b));
+}
+__device__ __forceinline__ void stg_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d));
+}
+__device__ __forceinline__ void stg_zero4_cg(void* p) {
+  asm volatile("st.global.cg.v4.b32 [%0], {%1, %1, %1, %1};" ::"l"(p), "r"(0));
+}
+__device__ __forceinline__ unsigned short bf16_bits(float x) {
+  __nv_bfloat16 h = __float2bfloat16_rn(x);
+  return *reinterpret_cast<unsigned short*>(&h);
+}
+
 // ------------------------------------------------------------------------------- element access
 // 16-byte vectors: 4 fp32 or 8 bf16 channels. All views have 16 B-aligned pixels/channel offsets.
 struct Vec8 {
@@ -229,14 +257,14 @@ __device__ __forceinline__ void load_vec(const View& vw, int dtype, int64_t pix,
 
 __device__ __forceinline__ void store_vec(const View& vw, int dtype, int64_t pix, int c, const float* in) {
   if (dtype != ET_BF16) {
-    float4 a = make_float4(rnd(in[0], dtype), rnd(in[1], dtype), rnd(in[2], dtype), rnd(in[3], dtype));
-    *reinterpret_cast<float4*>(reinterpret_cast<float*>(vw.ptr) + pix * vw.cstride + vw.coff + c) = a;
+    stg_v4(reinterpret_cast<float*>(vw.ptr) + pix * vw.cstride + vw.coff + c, __float_as_uint(rnd(in[0], dtype)),
+           __float_as_uint(rnd(in[1], dtype)), __float_as_uint(rnd(in[2], dtype)), __float_as_uint(rnd(in[3], dtype)));
   } else {
     uint4 a;
     __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&a);
 #pragma unroll
     for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(in[2 * i], in[2 * i + 1]);
-    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(vw.ptr) + pix * vw.cstride + vw.coff + c) = a;
+    stg_v4(reinterpret_cast<__nv_bfloat16*>(vw.ptr) + pix * vw.cstride + vw.coff + c, a.x, a.y, a.z, a.w);
   }
 }
 
@@ -248,9 +276,9 @@ __device__ __forceinline__ float load_elem(const View& vw, int dtype, int64_t pi
 }
 __device__ __forceinline__ void store_elem(const View& vw, int dtype, int64_t pix, int c, float x) {
   if (dtype != ET_BF16)
-    reinterpret_cast<float*>(vw.ptr)[pix * vw.cstride + vw.coff + c] = rnd(x, dtype);
+    stg_f32(reinterpret_cast<float*>(vw.ptr) + pix * vw.cstride + vw.coff + c, rnd(x, dtype));
   else
-    reinterpret_cast<__nv_bfloat16*>(vw.ptr)[pix * vw.cstride + vw.coff + c] = __float2bfloat16_rn(x);
+    stg_b16(reinterpret_cast<__nv_bfloat16*>(vw.ptr) + pix * vw.cstride + vw.coff + c, bf16_bits(x));
 }
 
 // ------------------------------------------------------------------------------ dependency waits
@@ -269,6 +297,21 @@ __device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* 
   }
 }
 
+// split-K rendezvous: every split of an output tile arrives after its reductions, then waits for
+// all `n` (the splits of one tile run on distinct, co-resident CTAs; a tile's splits only wait for
+// tiles with higher indices, which the CTAs reach after finishing lower ones: no cycle)
+__device__ __forceinline__ void split_rendezvous(int* ctr, int n, int* err) {
+  atom_acqrel_add(ctr, 1);
+  long long t0 = clock64();
+  while (ld_acquire(ctr) < n) {
+    __nanosleep(32);
+    if (clock64() - t0 > (long long)8000000000LL) {
+      atomicExch(err, 1);
+      break;
+    }
+  }
+}
+
 // -------------------------------------------------------------------------------- SIMT tile body
 // Memory-bound members. Items are (output pixel, 16 B channel vector); consecutive
 // threads take consecutive vectors of one pixel (coalesced). Code size matters as much as ILP
@@ -279,6 +322,163 @@ __device__ __forceinline__ void ld16(const View& vw, int64_t pix, int c, float* 
   load_vec(vw, DT, pix, c, out, DT == ET_BF16 ? 8 : 4);
 }
 
+// Window ops with a square k x k window (k in {3, 5, 7}) and stride s in {1, 2}: each item is a
+// quad of QW horizontally adjacent output pixels x one 16 B channel vector. Per window row the
+// thread loads the (QW-1)*s + k input pixels the quad needs, all in flight at once, and reuses
+// each for up to k taps x QW outputs (the generic path reloads every tap of every output).
+// KIND 0: sepconv front half ReLU(sum_i w_i x_i) -> depthwise (weights tap-major [k*k][C] fp32);
+// KIND 1: max pool (padding = -inf); KIND 2: avg pool (divisor per output as the generic path).
+template <int DT>
+constexpr int win_qw() { return DT == ET_BF16 ? 2 : 4; }
+
+template <int DT, int K, int S, int KIND>
+__device__ __noinline__ void win_tile(const Problem& P, const View* views, int tile, int tid, int nthr) {
+  constexpr int NV = DT == ET_BF16 ? 8 : 4;
+  constexpr int QW = win_qw<DT>();
+  constexpr int SPAN = (QW - 1) * S + K;
+  // descriptor fields and views by value (registers / local memory): no descriptor re-loads
+  // behind this tile's global stores
+  const View out = P.out;
+  const View in = views[P.in_begin];
+  const int nvec = out.C / NV;
+  const int item0 = tile * P.items_per_tile;
+  const int item1 = min(item0 + P.items_per_tile, P.n_items);
+  const int total = (item1 - item0) * nvec;
+  const int Ho = P.Ho, Wo = P.Wo, ph = P.ph, pw = P.pw, flags = P.flags;
+  const int wq = (Wo + QW - 1) / QW;
+  const int cs = in.C;
+  const float* wd = reinterpret_cast<const float*>(P.wts);
+  const int nin = KIND == 0 ? min(P.n_in, 8) : 1;
+  View vin[KIND == 0 ? 8 : 1];
+  float awv[KIND == 0 ? 8 : 1];
+  if (KIND == 0) {
+    const float* aw = reinterpret_cast<const float*>(P.add_w);
+    for (int s = 0; s < nin; ++s) {
+      vin[s] = views[P.in_begin + s];
+      awv[s] = aw ? __ldg(aw + s) : 1.0f;
+    }
+  }
+  const float neutral = KIND == 1 ? -INFINITY : 0.f;
+  for (int idx = tid; idx < total; idx += nthr) {
+    const int qi = idx / nvec;
+    const int c = (idx - qi * nvec) * NV;
+    const int q = item0 + qi;
+    const int row = q / wq;                       // n * Ho + oh
+    const int ow0 = (q - row * wq) * QW;
+    const int n = row / Ho, oh = row - n * Ho;
+    const int hs = oh * S - ph, ws = ow0 * S - pw;
+    float acc[QW][NV];
+#pragma unroll
+    for (int u = 0; u < QW; ++u)
+#pragma unroll
+      for (int e = 0; e < NV; ++e) acc[u][e] = neutral;
+    for (int i = 0; i < K; ++i) {
+      const int ih = hs + i;
+      if ((unsigned)ih >= (unsigned)in.H) continue;
+      const int64_t rowpix = ((int64_t)n * in.H + ih) * in.W + ws;
+      float xr[SPAN][NV];
+      if (KIND == 0 && nin > 1) {
+#pragma unroll
+        for (int t = 0; t < SPAN; ++t)
+#pragma unroll
+          for (int e = 0; e < NV; ++e) xr[t][e] = 0.f;
+        for (int s = 0; s < nin; ++s) {
+          const View& vs = vin[s];
+          const float w = awv[s];
+#pragma unroll
+          for (int t = 0; t < SPAN; ++t) {
+            if ((unsigned)(ws + t) < (unsigned)in.W) {
+              float x[NV];
+              ld16<DT>(vs, rowpix + t, c, x);
+#pragma unroll
+              for (int e = 0; e < NV; ++e) xr[t][e] = fmaf(w, x[e], xr[t][e]);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < SPAN; ++t) {
+          if ((unsigned)(ws + t) < (unsigned)in.W) {
+            ld16<DT>(in, rowpix + t, c, xr[t]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < NV; ++e) xr[t][e] = neutral;
+          }
+        }
+      }
+      if (KIND == 0) {
+#pragma unroll
+        for (int t = 0; t < SPAN; ++t)
+#pragma unroll
+          for (int e = 0; e < NV; ++e) xr[t][e] = fmaxf(xr[t][e], 0.f);   // padding stays 0
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          float w[NV];
+          const float4* wp = reinterpret_cast<const float4*>(wd + (int64_t)(i * K + j) * cs + c);
+#pragma unroll
+          for (int h = 0; h < NV / 4; ++h) {
+            const float4 v = __ldg(wp + h);
+            w[4 * h] = v.x; w[4 * h + 1] = v.y; w[4 * h + 2] = v.z; w[4 * h + 3] = v.w;
+          }
+#pragma unroll
+          for (int u = 0; u < QW; ++u)
+#pragma unroll
+            for (int e = 0; e < NV; ++e) acc[u][e] = fmaf(w[e], xr[u * S + j][e], acc[u][e]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+#pragma unroll
+          for (int u = 0; u < QW; ++u)
+#pragma unroll
+            for (int e = 0; e < NV; ++e)
+              acc[u][e] = KIND == 1 ? fmaxf(acc[u][e], xr[u * S + j][e]) : acc[u][e] + xr[u * S + j][e];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < QW; ++u) {
+      const int ow = ow0 + u;
+      if (ow >= Wo) break;
+      if (KIND == 2) {
+        const int wsu = ws + u * S;
+        const int he = min(hs + K, in.H + ph), we = min(wsu + K, in.W + pw);
+        int div;
+        if (flags & 8) div = (he - hs) * (we - wsu);
+        else div = (min(he, in.H) - max(hs, 0)) * (min(we, in.W) - max(wsu, 0));
+        const float inv = 1.0f / (float)div;
+#pragma unroll
+        for (int e = 0; e < NV; ++e) acc[u][e] *= inv;
+      }
+      store_vec(out, DT, (int64_t)row * Wo + ow, c, acc[u]);
+    }
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ bool win_dispatch(const Problem& P, const View* views, int tile, int tid, int nthr) {
+  const int k = P.kh, s = P.sh;
+  if (P.kind == PK_DWCONV) {
+    if (k == 3 && s == 1) win_tile<DT, 3, 1, 0>(P, views, tile, tid, nthr);
+    else if (k == 3 && s == 2) win_tile<DT, 3, 2, 0>(P, views, tile, tid, nthr);
+    else if (k == 5 && s == 1) win_tile<DT, 5, 1, 0>(P, views, tile, tid, nthr);
+    else if (k == 5 && s == 2) win_tile<DT, 5, 2, 0>(P, views, tile, tid, nthr);
+    else if (k == 7 && s == 1) win_tile<DT, 7, 1, 0>(P, views, tile, tid, nthr);
+    else if (k == 7 && s == 2) win_tile<DT, 7, 2, 0>(P, views, tile, tid, nthr);
+    else return false;
+  } else if (P.kind == PK_MAXPOOL && k == 3) {
+    if (s == 1) win_tile<DT, 3, 1, 1>(P, views, tile, tid, nthr);
+    else if (s == 2) win_tile<DT, 3, 2, 1>(P, views, tile, tid, nthr);
+    else return false;
+  } else if (P.kind == PK_AVGPOOL && k == 3) {
+    if (s == 1) win_tile<DT, 3, 1, 2>(P, views, tile, tid, nthr);
+    else if (s == 2) win_tile<DT, 3, 2, 2>(P, views, tile, tid, nthr);
+    else return false;
+  } else {
+    return false;
+  }
+  return true;
+}
+
 template <int DT>
 __device__ __noinline__ void simt_tile(const Problem& P, const View* views, int tile, int tid, int nthr) {
   constexpr int NV = DT == ET_BF16 ? 8 : 4;
@@ -286,36 +486,78 @@ __device__ __noinline__ void simt_tile(const Problem& P, const View* views, int 
   const int nvec = out.C / NV;
   const int item0 = tile * P.items_per_tile;
   const int item1 = min(item0 + P.items_per_tile, P.n_items);
+  if (P.dwq) {
+    win_dispatch<DT>(P, views, tile, tid, nthr);   // the planner set dwq only for supported shapes
+    return;
+  }
   if (P.kind == PK_GAVGPOOL) {
+    // 16 (image, channel vector) items per tile on warps 0-3: lane = (pixel phase p, item il);
+    // 8 pixel phases per item, 4 loads in flight per lane, shuffle-reduced over the phases
+    if (tid >= 128) return;
     const View& in = views[P.in_begin];
     const int hw = in.H * in.W;
     const float inv = 1.0f / (float)hw;
     const bool relu = (P.flags & 2) != 0;
-    for (int idx = item0 + tid; idx < item1; idx += nthr) {
-      const int n = idx / nvec, v = idx % nvec;
-      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int p0 = 0; p0 < hw; p0 += 4) {
-        float x0[8], x1[8], x2[8], x3[8];
-        const int64_t b = (int64_t)n * hw + p0;
-        ld16<DT>(in, b, v * NV, x0);
-        if (p0 + 1 < hw) ld16<DT>(in, b + 1, v * NV, x1);
-        if (p0 + 2 < hw) ld16<DT>(in, b + 2, v * NV, x2);
-        if (p0 + 3 < hw) ld16<DT>(in, b + 3, v * NV, x3);
+    const int lane = tid & 31, il = lane & 3, p = lane >> 2;
+    const int idx = item0 + (tid >> 5) * 4 + il;
+    const bool ok = idx < item1;
+    const int n = ok ? idx / nvec : 0, v = ok ? idx - (idx / nvec) * nvec : 0;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (ok) {
+      for (int p0 = p; p0 < hw; p0 += 32) {
+        float x[4][8];
 #pragma unroll
-        for (int e = 0; e < NV; ++e) {
-          acc[e] += relu ? fmaxf(x0[e], 0.f) : x0[e];
-          if (p0 + 1 < hw) acc[e] += relu ? fmaxf(x1[e], 0.f) : x1[e];
-          if (p0 + 2 < hw) acc[e] += relu ? fmaxf(x2[e], 0.f) : x2[e];
-          if (p0 + 3 < hw) acc[e] += relu ? fmaxf(x3[e], 0.f) : x3[e];
-        }
+        for (int u = 0; u < 4; ++u)
+          if (p0 + 8 * u < hw) ld16<DT>(in, (int64_t)n * hw + p0 + 8 * u, v * NV, x[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (p0 + 8 * u < hw) {
+#pragma unroll
+            for (int e = 0; e < NV; ++e) acc[e] += relu ? fmaxf(x[u][e], 0.f) : x[u][e];
+          }
       }
-#pragma unroll
-      for (int e = 0; e < NV; ++e) acc[e] *= inv;
-      store_vec(out, DT, n, v * NV, acc);
     }
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 4);
+      acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 8);
+      acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+      acc[e] *= inv;
+    }
+    if (ok && p == 0) store_vec(out, DT, n, v * NV, acc);
     return;
   }
   const int total = (item1 - item0) * nvec;
+  if (P.kind == PK_ADD && P.n_in <= 8) {
+    // n-ary weighted add: inputs and weights by value (no descriptor re-loads behind the stores),
+    // all inputs of an item loaded before the sum
+    const View o = out;
+    const int nin = P.n_in;
+    View vin[8];
+    float awv[8];
+    const float* aw = reinterpret_cast<const float*>(P.add_w);
+    for (int i = 0; i < nin; ++i) {
+      vin[i] = views[P.in_begin + i];
+      awv[i] = aw ? __ldg(aw + i) : 1.0f;
+    }
+    for (int idx = tid; idx < total; idx += nthr) {
+      const int pix = item0 + idx / nvec;
+      const int c = (idx % nvec) * NV;
+      float x[8][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < nin) ld16<DT>(vin[i], pix, c, x[i]);
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < nin) {
+#pragma unroll
+          for (int e = 0; e < NV; ++e) acc[e] = fmaf(awv[i], x[i][e], acc[e]);
+        }
+      store_vec(o, DT, pix, c, acc);
+    }
+    return;
+  }
   const int HoWo = P.Ho * P.Wo;
   const float* aw = reinterpret_cast<const float*>(P.add_w);
   for (int idx = tid; idx < total; idx += nthr) {
@@ -369,13 +611,13 @@ __device__ __noinline__ void simt_tile(const Problem& P, const View* views, int 
             }
           }
           if (is_dw) {
-            const int kk = P.kh * P.kw, tap = i * P.kw + j0;
+            const int tap = i * P.kw + j0, cs = in.C;   // weights tap-major [kh*kw][C]
 #pragma unroll
             for (int e = 0; e < NV; ++e) {
-              const float* we = wd + (c + e) * kk + tap;
+              const float* we = wd + (int64_t)tap * cs + c + e;
               if (v0) acc[e] = fmaf(__ldg(we), fmaxf(a0[e], 0.f), acc[e]);
-              if (v1) acc[e] = fmaf(__ldg(we + 1), fmaxf(a1[e], 0.f), acc[e]);
-              if (v2) acc[e] = fmaf(__ldg(we + 2), fmaxf(a2[e], 0.f), acc[e]);
+              if (v1) acc[e] = fmaf(__ldg(we + cs), fmaxf(a1[e], 0.f), acc[e]);
+              if (v2) acc[e] = fmaf(__ldg(we + 2 * cs), fmaxf(a2[e], 0.f), acc[e]);
             }
           } else {
 #pragma unroll
@@ -436,7 +678,10 @@ __device__ __forceinline__ int find_problem(const int* sm_tile_begin, int n_prob
   return p;
 }
 
-template <int DT>
+// SD: the descriptor table fits the smem copy (the host picks the instantiation). The pointers are
+// then derived from the shared array, so descriptor reads compile to shared loads, which do not
+// wait behind outstanding global stores the way generic loads do.
+template <int DT, bool SD>
 __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc sd) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -456,8 +701,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 
   // The descriptor table is copied into shared memory once, so every role decodes its tiles from
   // smem instead of a chain of dependent global loads.
-  const bool desc_in_smem = sd.blob_bytes <= kDescBytes;
-  const uint8_t* dbase = desc_in_smem ? sdesc : reinterpret_cast<const uint8_t*>(sd.problems);
+  constexpr bool desc_in_smem = SD;
+  const uint8_t* dbase = SD ? sdesc : reinterpret_cast<const uint8_t*>(sd.problems);
   const Problem* probs = reinterpret_cast<const Problem*>(dbase);
   const View* views = reinterpret_cast<const View*>(dbase + sd.views_off);
   const Segment* segs = reinterpret_cast<const Segment*>(dbase + sd.segs_off);
@@ -569,10 +814,13 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const int nt = rest - mt * P.n_tiles_n;
       const int c0 = s * P.chunks_per_split;
       const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
-      if (P.a_tma) {
+      if (P.a_tma || P.tt) {
         // A is a plain [M, C] matrix (1x1, stride 1): ONE tensor TMA per chunk (128 rows x 128 B,
         // 128 B swizzle, rows past M / channels past C zero-filled) + one bulk copy for B, both
         // issued by one thread; warps 1-3 only keep their ring position in step.
+        // Tap TMA (P.tt): chunk c = (tap, channel block); ONE 4D tensor TMA brings that tap's input
+        // pixels of the tile's output patch (element strides = conv strides; padding and channels
+        // past C are out-of-bounds zeros) in the same 128 B-swizzled [row][128 B] layout.
         if (warp == 0) {
           const uint64_t tmap = P.tmap_a;
           const bool swap = P.swap_ab != 0;
@@ -585,12 +833,34 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           uint8_t* const xbuf = swap ? sB : sA;
           const int wsb = swap ? kAStageBytes : kBStageBytes, xsb = swap ? kBStageBytes : kAStageBytes;
           const int xrow0 = swap ? 0 : mt * kBM;
+          // tap-TMA patch origin (input coordinates of tap (0, 0)) and box bytes
+          int tn0 = 0, ih0 = 0, iw0 = 0;
+          uint32_t xbytes = kAStageBytes;
+          const int kblk = P.kblk, kwid = P.kw;
+          if (P.tt) {
+            const int rr = fdiv(P.fd_tilw, swap ? 0 : mt);
+            const int tw = (swap ? 0 : mt) - rr * P.tiles_w;
+            const int tnn = fdiv(P.fd_tilh, rr);
+            const int th = rr - tnn * P.tiles_h;
+            tn0 = tnn * P.tN;
+            ih0 = th * P.tR * P.sh - P.ph;
+            iw0 = tw * P.tWt * P.sw - P.pw;
+            xbytes = (uint32_t)(P.tN * P.tR * P.tWt) * kChunkBytes;
+          }
           for (int c = c0; c < c1; ++c) {
             mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
             if (lane == 0) {
               const uint32_t fb = smem_u32(&full[ring.slot]);
-              mbar_arrive_expect_tx(fb, kAStageBytes + bbytes);
-              tma_load_2d(smem_u32(xbuf + ring.slot * xsb), tmap, c * ELEMS, xrow0, fb);
+              mbar_arrive_expect_tx(fb, xbytes + bbytes);
+              if (P.tt) {
+                const int tap = fdiv(P.fd_kblk, c);
+                const int cb = c - tap * kblk;
+                const int ti = fdiv(P.fd_kw, tap);
+                const int tj = tap - ti * kwid;
+                tma_load_4d(smem_u32(xbuf + ring.slot * xsb), tmap, cb * ELEMS, iw0 + tj, ih0 + ti, tn0, fb);
+              } else {
+                tma_load_2d(smem_u32(xbuf + ring.slot * xsb), tmap, c * ELEMS, xrow0, fb);
+              }
               bulk_g2s(smem_u32(wbuf + ring.slot * wsb), wsrc + c * wstep, bbytes, fb);
               mbar_arrive_cnt(fb, kProducerWarps);   // stands in for the 4 producer warps' arrivals
               if (tfirst && c - c0 < 3) IOS_TRACE(c == c0 ? 2 : 8 + c - c0);
@@ -649,6 +919,33 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       uint8_t* const xbuf = swap ? sB : sA;
       const int wsb = swap ? kAStageBytes : kBStageBytes, xsb = swap ? kBStageBytes : kAStageBytes;
       const char* ibase = reinterpret_cast<const char*>(in.ptr) + (int64_t)in.coff * ESZ;
+      // pre-ReLU convs: the gather stays asynchronous; once a chunk's copies have landed, each thread
+      // applies the ReLU in place to the 8 pieces it copied itself (visible to it after wait_group)
+      auto relu_pieces = [&](int slot) {
+        const uint32_t b0 = smem_u32(xbuf + slot * xsb) + rig * 16 + pc0 * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (roff[j] == INT_MIN) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t a = b0 + (warp + 4 * j) * 1024 + h * 512;
+            uint32_t w[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(a));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (ESZ == 4) {
+                w[q] = __float_as_uint(fmaxf(__uint_as_float(w[q]), 0.f));
+              } else {
+                __nv_bfloat162 hb = *reinterpret_cast<__nv_bfloat162*>(&w[q]);
+                hb = __hmax2(hb, __floats2bfloat162_rn(0.f, 0.f));
+                w[q] = *reinterpret_cast<uint32_t*>(&hb);
+              }
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                         : "memory");
+          }
+        }
+      };
       int pend[2] = {-1, -1};
       for (int c = c0; c < c1; ++c) {
         mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
@@ -670,22 +967,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             // padding taps / K tail: zero fill without reading (ignore-src)
             const char* src = ibase + ((int64_t)roff[j] * cstride + (ok ? toff : 0)) * ESZ;
             const uint32_t dst = a_st + (warp + 4 * j) * 1024 + h * 512;
-            if (!relu_pre) {
-              cp_async16_zfill(dst, ok ? src : ibase, !ok);
-            } else {
-              uint4 v = make_uint4(0, 0, 0, 0);
-              if (ok) v = __ldcg(reinterpret_cast<const uint4*>(src));
-              if (ESZ == 4) {
-                float* f = reinterpret_cast<float*>(&v);
-                f[0] = fmaxf(f[0], 0.f); f[1] = fmaxf(f[1], 0.f); f[2] = fmaxf(f[2], 0.f); f[3] = fmaxf(f[3], 0.f);
-              } else {
-                __nv_bfloat162* hb = reinterpret_cast<__nv_bfloat162*>(&v);
-                const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
-                hb[0] = __hmax2(hb[0], z); hb[1] = __hmax2(hb[1], z); hb[2] = __hmax2(hb[2], z); hb[3] = __hmax2(hb[3], z);
-              }
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(v.x), "r"(v.y), "r"(v.z),
-                           "r"(v.w) : "memory");
-            }
+            cp_async16_zfill(dst, ok ? src : ibase, !ok);
           }
           // advance this piece by one chunk (ELEMS elements of K)
           ci[h] += ELEMS;
@@ -702,6 +984,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // arrive for the chunk issued two iterations ago (keeps up to 3 chunks of cp.async in flight)
         if (pend[0] >= 0) {
           cp_async_wait<2>();
+          if (relu_pre) relu_pieces(pend[0]);
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&full[pend[0]]));   // one arrival per producer warp
@@ -711,6 +994,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         ring.next();
       }
       cp_async_wait<0>();
+      if (relu_pre) {
+        if (pend[0] >= 0) relu_pieces(pend[0]);
+        if (pend[1] >= 0) relu_pieces(pend[1]);
+      }
       if (ptid == 0 && tfirst) IOS_TRACE(12);
       tfirst = false;
       fence_proxy_async();
@@ -739,8 +1026,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
         const uint32_t idesc = umma_idesc(DT == ET_BF16, P.BN);
         // the activation operand is 128 B-swizzled when TMA loads it; swap-AB puts it in the B slot
-        const bool a_sw128 = P.a_tma != 0 && !P.swap_ab;
-        const bool b_sw128 = P.a_tma != 0 && P.swap_ab;
+        const bool act_tma = P.a_tma != 0 || P.tt != 0;
+        const bool a_sw128 = act_tma && !P.swap_ab;
+        const bool b_sw128 = act_tma && P.swap_ab;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)acc * kMaxBN;
@@ -793,8 +1081,33 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const int s = local - rest * P.split;
       const int mt = fdiv(P.fd_ntn, rest);
       const int nt = rest - mt * P.n_tiles_n;
-      const int m = mt * kBM + etid;
-      const bool valid = m < P.M;
+      // tile row -> output pixel (-1: none). Dense tiles: 128 consecutive pixels. Tap-TMA tiles:
+      // a tN x tR x tWt output patch, row r = (nn * tR + i) * tWt + j.
+      int tn0 = 0, toh0 = 0, tow0 = 0;
+      if (P.tt) {
+        const int rr = fdiv(P.fd_tilw, mt);
+        const int tw = mt - rr * P.tiles_w;
+        const int tnn = fdiv(P.fd_tilh, rr);
+        tn0 = tnn * P.tN;
+        toh0 = (rr - tnn * P.tiles_h) * P.tR;
+        tow0 = tw * P.tWt;
+      }
+      const int trows = P.tt ? P.tN * P.tR * P.tWt : min(kBM, P.M - mt * kBM);
+      // everything the store loops need is copied into registers: the descriptors are read through
+      // generic pointers, and a descriptor re-load behind a global store waits for that store
+      const bool is_tt = P.tt != 0;
+      const FastDiv fthw = P.fd_thw, ftw = P.fd_tw;
+      const int thw = P.tR * P.tWt, tWt = P.tWt, nb = P.batch, Ho = P.Ho, Wo = P.Wo, Mx = P.M, BNx = P.BN;
+      auto pixel = [=](int r) -> int {
+        if (!is_tt) return r < trows ? mt * kBM + r : -1;
+        const int nn = fdiv(fthw, r);
+        const int rem = r - nn * thw;
+        const int i = fdiv(ftw, rem);
+        const int n = tn0 + nn, oh = toh0 + i, ow = tow0 + rem - i * tWt;
+        return (r < trows && n < nb && oh < Ho && ow < Wo) ? (n * Ho + oh) * Wo + ow : -1;
+      };
+      const int m = pixel(etid);
+      const bool valid = m >= 0;
       const int esz_out = P.dtype == ET_BF16 ? 2 : 4;
       const float* bias = reinterpret_cast<const float*>(P.bias);
       if (P.swap_ab) {
@@ -808,82 +1121,119 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         }
         const float bv = sgp ? __ldg(bias + ch) : 0.f;
         const int relu = sgp ? sgp->relu : 0;
-        char* ocol = sgp ? reinterpret_cast<char*>(sgp->out.ptr) +
-                               ((int64_t)sgp->out.coff + ch - sgp->n0) * (DT == ET_BF16 ? 2 : 4)
-                         : nullptr;
-        const int64_t ostride = sgp ? (int64_t)sgp->out.cstride * (DT == ET_BF16 ? 2 : 4) : 0;
+        // Output writes go through this warp's smem staging area as 16 B vectors along channels:
+        // per 4 pixels each thread stages its channel's 4 values ([pixel][32 channels]), then lane
+        // (pixel p, 16 B piece q) stores one vector. Lane q's destination comes from the segment of
+        // its own piece (segment boundaries are multiples of 8 channels).
+        constexpr int OESZ = DT == ET_BF16 ? 2 : 4;
+        constexpr int PPP = 32 * OESZ / 16;           // 16 B pieces per pixel row of 32 channels (8 / 4)
+        const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
+        const int sp = lane / PPP, sq = lane % PPP;   // store lane -> (pixel in the group, piece)
+        char* qptr = nullptr;
+        int64_t qstride = 0;
+        {
+          const int qch = mt * kBM + (warp & 3) * 32 + sq * (16 / OESZ);
+          for (int q = 0; q < P.n_seg; ++q) {
+            const Segment& sg = segs[P.seg_begin + q];
+            if (qch >= sg.n0 && qch < sg.n1) {
+              qptr = reinterpret_cast<char*>(sg.out.ptr) + ((int64_t)sg.out.coff + qch - sg.n0) * OESZ;
+              qstride = (int64_t)sg.out.cstride * OESZ;
+            }
+          }
+        }
+        // stage 4 pixels (px0 .. px0+3) of this thread's channel, then store them as vectors
+        auto emit4 = [&](int px0, const float* o) {
+          if (DT == ET_BF16) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(stg + (e * 32 + lane) * 2), "h"(bf16_bits(o[e])));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (e * 32 + lane) * 4), "r"(__float_as_uint(rnd(o[e], DT))));
+          }
+          __syncwarp();
+          if (sp < 4 && qptr && px0 + sp < Mx) {
+            uint32_t w0, w1, w2, w3;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                         : "r"(stg + sp * 32 * OESZ + sq * 16));
+            stg_v4(qptr + (int64_t)(px0 + sp) * qstride, w0, w1, w2, w3);
+          }
+          __syncwarp();
+        };
         mbar_wait(smem_u32(&tfull[acc]), acc_phase);
         if (etid == 0 && tfirst) IOS_TRACE(5);
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
         const int out_tile = mt;
         if (P.split == 1) {
-          for (int c0 = 0; c0 < P.BN; c0 += 16) {
+          for (int c0 = 0; c0 < BNx && c0 < Mx; c0 += 16) {
             uint32_t v[16];
             tmem_ld16(tbase + c0, v);
             tmem_ld_wait();
-            if (!sgp) continue;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int px = c0 + j;
-              if (px >= P.M) break;
-              float o = __uint_as_float(v[j]) + bv;
-              if (relu) o = fmaxf(o, 0.f);
-              if (DT == ET_BF16)
-                *reinterpret_cast<__nv_bfloat16*>(ocol + px * ostride) = __float2bfloat16_rn(o);
-              else
-                *reinterpret_cast<float*>(ocol + px * ostride) = rnd(o, DT);
+            for (int g4 = 0; g4 < 4; ++g4) {
+              if (c0 + 4 * g4 >= Mx) break;
+              float o[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                o[e] = __uint_as_float(v[4 * g4 + e]) + bv;
+                if (relu) o[e] = fmaxf(o[e], 0.f);
+              }
+              emit4(c0 + 4 * g4, o);
             }
           }
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty[acc]));
         } else {
-          // split-K: fp32 accumulator [pixel][128 channels]; coalesced scalar reductions
-          float* tacc = reinterpret_cast<float*>(P.workspace) + (int64_t)out_tile * kBM * P.BN;
-          for (int c0 = 0; c0 < P.BN; c0 += 16) {
+          // split-K: fp32 accumulator channel-major [128 channels][BN pixels]; each thread adds its
+          // channel's 16 pixels per TMEM load with four 16 B vector reductions (pixels past M add 0)
+          float* tacc = reinterpret_cast<float*>(P.workspace) + (int64_t)out_tile * kBM * BNx;
+          float* trow = tacc + (int64_t)etid * BNx;
+          for (int c0 = 0; c0 < BNx; c0 += 16) {
             uint32_t v[16];
             tmem_ld16(tbase + c0, v);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int px = c0 + j;
-              if (px < P.M)
-                asm volatile("red.global.add.f32 [%0], %1;" ::"l"(tacc + px * kBM + etid), "r"(v[j]) : "memory");
-            }
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j >= Mx) v[j] = 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (c0 + 4 * q < Mx)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(trow + c0 + 4 * q), "r"(v[4 * q]),
+                             "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3]));
           }
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty[acc]));
           named_bar(2, 128);
-          if (etid == 0) {
-            const int old = atom_acqrel_add(counters + P.tilectr_idx + out_tile, 1);
-            *flag = (old == P.split - 1);
-          }
+          if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err);
           named_bar(2, 128);
-          if (*flag == 0) {
-            tfirst = false;
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1u;
-            continue;
-          }
-          for (int p0 = 0; p0 < P.M; p0 += 8) {
-            float x[8];
+          // distributed finalize: split s owns pixel quads [s*np4/S, (s+1)*np4/S) of the tile; each
+          // thread reads its channel's quads (float4, 8 in flight), re-zeroes them, and emits them
+          // through the staged vector stores. Reading lines other SMs just reduced into is slow,
+          // so the S splits share the read-back instead of one last-arriving CTA doing it all.
+          const int np4 = (Mx + 3) >> 2;
+          const int kq0 = s * np4 / P.split, kq1 = (s + 1) * np4 / P.split;
+          if (etid == 0) IOS_TRACE(13);
+          for (int k0 = kq0; k0 < kq1; k0 += 8) {
+            float4 x[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-              if (p0 + u < P.M) x[u] = __ldcg(tacc + (p0 + u) * kBM + etid);
+              if (k0 + u < kq1) x[u] = __ldcg(reinterpret_cast<const float4*>(trow) + k0 + u);
+            if (etid == 0 && k0 == kq0) IOS_TRACE(14);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              const int px = p0 + u;
-              if (px >= P.M) break;
-              __stcg(tacc + px * kBM + etid, 0.f);
-              if (!sgp) continue;
-              float o = x[u] + bv;
-              if (relu) o = fmaxf(o, 0.f);
-              if (DT == ET_BF16)
-                *reinterpret_cast<__nv_bfloat16*>(ocol + px * ostride) = __float2bfloat16_rn(o);
-              else
-                *reinterpret_cast<float*>(ocol + px * ostride) = rnd(o, DT);
+              if (k0 + u >= kq1) break;
+              stg_zero4_cg(reinterpret_cast<float4*>(trow) + k0 + u);
+              float o[4] = {x[u].x + bv, x[u].y + bv, x[u].z + bv, x[u].w + bv};
+              if (relu) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[e] = fmaxf(o[e], 0.f);
+              }
+              emit4((k0 + u) * 4, o);
             }
           }
+          if (etid == 0) IOS_TRACE(15);
         }
         if (P.signal) {
           named_bar(2, 128);
@@ -902,7 +1252,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       if constexpr (DT == ET_F32X) {
         const int c0 = s * P.chunks_per_split;
         const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
-        const int bn = P.BN;
+        const int bn = BNx;
         for (int c = c0; c < c1; ++c) {
           mbar_wait(smem_u32(&full[ering.slot]), ering.phase);
           const uint8_t* As = sA + ering.slot * kAStageBytes + (etid >> 3) * 1024 + (etid & 7) * 16;
@@ -936,7 +1286,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       // stage this tile's bias slice in smem while the MMAs run (one load round trip, off the
       // critical path); the previous tile's readers of this buffer are past the barrier below
       float* sbias = sbias_all + acc * kMaxBN;
-      for (int i = etid; i < P.BN; i += 128) sbias[i] = __ldg(bias + nt * P.BN + i);
+      for (int i = etid; i < BNx; i += 128) sbias[i] = __ldg(bias + nt * BNx + i);
       named_bar(2, 128);
       if (DT != ET_F32X) mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       if (etid == 0 && tfirst) IOS_TRACE(5);
@@ -952,13 +1302,16 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         constexpr int PPR = 32 * OESZ / 16;                 // 16 B pieces per row per round (8 / 4)
         const Segment& sg = segs[P.seg_begin];
         const int relu = sg.relu;
-        const int ncols = min(P.BN, sg.n1 - nt * P.BN);     // valid columns of this tile
-        const int wrow0 = mt * kBM + (warp & 3) * 32;       // first tile row of this warp
+        const int ncols = min(BNx, sg.n1 - nt * BNx);     // valid columns of this tile
         char* obase = reinterpret_cast<char*>(sg.out.ptr) +
-                      ((int64_t)sg.out.coff + nt * P.BN - sg.n0) * OESZ;
+                      ((int64_t)sg.out.coff + nt * BNx - sg.n0) * OESZ;
         const int ocs = sg.out.cstride;
         const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
-        for (int c0 = 0; c0 < P.BN; c0 += 32) {
+        constexpr int RPI = 32 / PPR;                       // rows per write-out instruction (4 / 8)
+        int opix[32 / RPI];                                 // output pixel of each row this lane writes
+#pragma unroll
+        for (int it = 0; it < 32 / RPI; ++it) opix[it] = pixel((warp & 3) * 32 + it * RPI + lane / PPR);
+        for (int c0 = 0; c0 < BNx; c0 += 32) {
           uint32_t va[16], vb[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
           acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
@@ -989,17 +1342,15 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           __syncwarp();
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(14);
           // coalesced write-out: lane -> (row, piece)
-          constexpr int RPI = 32 / PPR;                     // rows per instruction (4 / 8)
 #pragma unroll
           for (int it = 0; it < 32 / RPI; ++it) {
             const int r = it * RPI + lane / PPR, p = lane % PPR;
             uint32_t w0, w1, w2, w3;
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
                          : "r"(stg + r * (PPR * 16) + ((p ^ (r & 7)) % PPR) * 16));
-            const int mrow = wrow0 + r;
             const int col = c0 + p * (16 / OESZ);
-            if (mrow < P.M && col < ncols)
-              *reinterpret_cast<uint4*>(obase + ((int64_t)mrow * ocs + col) * OESZ) = make_uint4(w0, w1, w2, w3);
+            if (opix[it] >= 0 && col < ncols)
+              stg_v4(obase + ((int64_t)opix[it] * ocs + col) * OESZ, w0, w1, w2, w3);
           }
           __syncwarp();
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(15);
@@ -1007,14 +1358,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         tc_fence_before();
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
       } else if (P.split == 1) {
-        for (int c0 = 0; c0 < P.BN; c0 += 16) {
+        for (int c0 = 0; c0 < BNx; c0 += 16) {
           uint32_t v[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, v);
           acc_wait<DT>();
           if (!valid) continue;
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
-            const int ncol = nt * P.BN + c0 + g * 8;
+            const int ncol = nt * BNx + c0 + g * 8;
             for (int q = 0; q < P.n_seg; ++q) {
               const Segment& sg = segs[P.seg_begin + q];
               if (ncol >= sg.n0 && ncol < sg.n1) {
@@ -1041,10 +1392,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // vector reductions (fire-and-forget at L2); the last arriving split reads the sum once,
         // applies bias/ReLU, stores, and re-zeroes the accumulator for the next launch.
         float* ws = reinterpret_cast<float*>(P.workspace);
-        float* tacc = ws + (int64_t)out_tile * kBM * P.BN;     // [kBM][BN] fp32 accumulator
+        float* tacc = ws + (int64_t)out_tile * kBM * BNx;     // [kBM][BN] fp32 accumulator
         const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
         const int wr0 = (warp & 3) * 32;
-        for (int c0 = 0; c0 < P.BN; c0 += 32) {
+        for (int c0 = 0; c0 < BNx; c0 += 32) {
           uint32_t va[16], vb[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
           acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
@@ -1064,27 +1415,24 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
                          : "r"(stg + r * 128 + ((p ^ (r & 7)) * 16)));
             const int col = c0 + p * 4;
-            if (mt * kBM + wr0 + r < P.M && col < P.BN)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(tacc + (wr0 + r) * P.BN + col),
-                           "r"(w0), "r"(w1), "r"(w2), "r"(w3) : "memory");
+            if (wr0 + r < trows && col < BNx)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(tacc + (wr0 + r) * BNx + col),
+                           "r"(w0), "r"(w1), "r"(w2), "r"(w3) );
           }
           __syncwarp();
         }
         tc_fence_before();
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
         named_bar(2, 128);
-        if (etid == 0) {
-          const int old = atom_acqrel_add(counters + P.tilectr_idx + out_tile, 1);
-          *flag = (old == P.split - 1);
-        }
+        if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err);
         named_bar(2, 128);
-        const bool last = *flag != 0;
-        if (last) {
-          // finalize the whole tile with all 128 threads, coalesced (consecutive threads sweep a
-          // row's contiguous columns), then re-zero the accumulator for the next launch
-          const int q4 = P.BN / 4;
-          const int rows = min(kBM, P.M - mt * kBM);
-          const int total = rows * q4;
+        {
+          // distributed finalize (see the swap-AB path): split s owns tile rows
+          // [s*trows/S, (s+1)*trows/S); all 128 threads, coalesced (consecutive threads sweep a
+          // row's contiguous columns), re-zeroing the accumulator for the next launch
+          const int bn = BNx, q4 = bn / 4;
+          const int r0 = s * trows / P.split, r1 = (s + 1) * trows / P.split;
+          const int total = (r1 - r0) * q4;
           // 8 independent float4 loads in flight per thread per round (the accumulator sits in L2)
           for (int base = etid; base < total; base += 128 * 8) {
             float4 x[8];
@@ -1092,17 +1440,17 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             for (int u = 0; u < 8; ++u) {
               const int idx = base + u * 128;
               if (idx < total) {
-                const int r = idx / q4, col = (idx - r * q4) * 4;
-                x[u] = __ldcg(reinterpret_cast<const float4*>(tacc + r * P.BN + col));
+                const int r = r0 + idx / q4, col = (idx % q4) * 4;
+                x[u] = __ldcg(reinterpret_cast<const float4*>(tacc + r * bn + col));
               }
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int idx = base + u * 128;
               if (idx >= total) break;
-              const int r = idx / q4, col = (idx - r * q4) * 4;
-              __stcg(reinterpret_cast<float4*>(tacc + r * P.BN + col), make_float4(0.f, 0.f, 0.f, 0.f));
-              const int ncol = nt * P.BN + col;
+              const int r = r0 + idx / q4, col = (idx % q4) * 4;
+              stg_zero4_cg(tacc + r * bn + col);
+              const int ncol = nt * bn + col;
               const Segment* sgp = &segs[P.seg_begin];
               if (P.n_seg > 1) {
                 for (int q = 0; q < P.n_seg; ++q)
@@ -1112,29 +1460,26 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
                   }
               }
               if (ncol < sgp->n0 || ncol >= sgp->n1) continue;
+              const int px = pixel(r);
+              if (px < 0) continue;
               float o[4] = {x[u].x + sbias[col], x[u].y + sbias[col + 1], x[u].z + sbias[col + 2], x[u].w + sbias[col + 3]};
               if (sgp->relu) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) o[e] = fmaxf(o[e], 0.f);
               }
-              const int64_t pix = (int64_t)mt * kBM + r;
+              const int64_t pix = px;
               if (DT == ET_BF16) {
                 __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
-                uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
-                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(sgp->out.ptr) + pix * sgp->out.cstride +
-                                          sgp->out.coff + ncol - sgp->n0) = pk;
+                stg_v2(reinterpret_cast<__nv_bfloat16*>(sgp->out.ptr) + pix * sgp->out.cstride + sgp->out.coff + ncol -
+                           sgp->n0,
+                       *reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
               } else {
-                *reinterpret_cast<float4*>(reinterpret_cast<float*>(sgp->out.ptr) + pix * sgp->out.cstride +
-                                           sgp->out.coff + ncol - sgp->n0) =
-                    make_float4(rnd(o[0], DT), rnd(o[1], DT), rnd(o[2], DT), rnd(o[3], DT));
+                stg_v4(reinterpret_cast<float*>(sgp->out.ptr) + pix * sgp->out.cstride + sgp->out.coff + ncol - sgp->n0,
+                       __float_as_uint(rnd(o[0], DT)), __float_as_uint(rnd(o[1], DT)), __float_as_uint(rnd(o[2], DT)),
+                       __float_as_uint(rnd(o[3], DT)));
               }
             }
           }
-        }
-        if (!last) {
-          acc ^= 1;
-          if (acc == 0) acc_phase ^= 1u;
-          continue;
         }
       }
       if (P.signal) {
@@ -1209,11 +1554,12 @@ __global__ void l2_flush_kernel(int4* buf, int64_t n) {
 cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(ios_stage_kernel<ET_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(ios_stage_kernel<ET_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(ios_stage_kernel<ET_F32X>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
+    const void* ks[6] = {(const void*)ios_stage_kernel<ET_F32, true>, (const void*)ios_stage_kernel<ET_F32, false>,
+                         (const void*)ios_stage_kernel<ET_BF16, true>, (const void*)ios_stage_kernel<ET_BF16, false>,
+                         (const void*)ios_stage_kernel<ET_F32X, true>, (const void*)ios_stage_kernel<ET_F32X, false>};
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 6 && e == cudaSuccess; ++i)
+      e = cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -1227,9 +1573,15 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (dtype == ET_BF16) return cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_BF16>, sd);
-  if (dtype == ET_F32X) return cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32X>, sd);
-  return cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32>, sd);
+  const bool smem_desc = sd.blob_bytes <= kDescBytes;
+  if (dtype == ET_BF16)
+    return smem_desc ? cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_BF16, true>, sd)
+                     : cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_BF16, false>, sd);
+  if (dtype == ET_F32X)
+    return smem_desc ? cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32X, true>, sd)
+                     : cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32X, false>, sd);
+  return smem_desc ? cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32, true>, sd)
+                   : cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32, false>, sd);
 }
 
 cudaError_t launch_nchw_to_nhwc(const float* in, const View& out, int dtype, int N, int C, cudaStream_t st) {

@@ -15,7 +15,7 @@ from typing import Callable, List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libios.so")
+LIB_PATH = os.environ.get("IOS_LIB") or os.path.join(_HERE, "libios.so")   # IOS_LIB: experiment builds
 
 IOS_OK = 0
 STATUS = {0: "IOS_OK", 1: "IOS_ERR_INVALID_ARG", 2: "IOS_ERR_DANGLING_INPUT", 3: "IOS_ERR_SHAPE", 4: "IOS_ERR_BLOCK",

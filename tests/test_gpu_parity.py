@@ -117,3 +117,22 @@ def test_fp32_simt_mode_1e5(torch_cuda, name):
     assert rel_err(y, ref) < 1e-5
     _, _, y2 = _run(net, "fp32_simt", "greedy", torch_cuda)
     assert rel_err(y2, ref) < 1e-5
+
+
+@pytest.mark.parametrize("batch,hw,math", [(1, 37, "tf32"), (1, 37, "bf16"), (3, 7, "tf32"), (2, 9, "bf16"),
+                                           (1, 150, "bf16")])
+def test_conv_zoo_im2col_paths(torch_cuda, batch, hw, math):
+    """Every conv shape class through the im2col paths (tap-TMA patches incl. multi-image and
+    multi-column-tile patches, the cp.async gather, 1x1 TMA): per op under the sequential schedule,
+    and the {3x3, 1x1, 5x5} group as one merged stage."""
+    from paper_2011_01302_b200 import MERGE
+    net = W.build("conv_zoo", batch=batch, hw=hw, math=math)
+    g, q, y = _run(net, math, "sequential", torch_cuda)
+    errs = per_op_errors(net, g, math)
+    worst = max(errs, key=errs.get)
+    assert errs[worst] < TOL[math], (worst, net.op(worst).name, errs[worst])
+    stages = [([i], 0) for i in range(1, 12)] + [([12, 13, 14], MERGE), ([15], 0)]
+    g.run(g.schedule(stages), torch_cuda.from_numpy(net.make_input()).cuda())
+    torch_cuda.cuda.synchronize()
+    errs = per_op_errors(net, g, math, ops=[12, 13, 14])
+    assert max(errs.values()) < TOL[math], errs

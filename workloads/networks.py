@@ -71,6 +71,30 @@ def tiny_mixed_net(seed: int = 7, batch: int = 1, math: str = "tf32", hw: int = 
     return nb.net
 
 
+def conv_zoo_net(seed: int = 11, batch: int = 1, math: str = "tf32", hw: int = 37, cin: int = 48) -> NetSpec:
+    """Conv shape zoo (parity tests of the im2col paths; not a paper workload): square / asymmetric
+    kernels, strides 1-3, zero and non-zero padding, chained convs and one mergeable group."""
+    nb = NetBuilder("conv_zoo", (batch, cin, hw, hw), seed, math)
+    nb.new_block()
+    a = nb.conv(0, 48, 3, 1, 1, name="k3s1p1")
+    nb.conv(0, 40, 3, 2, 0, name="k3s2p0")
+    nb.conv(0, 32, 5, 1, 2, name="k5s1p2")
+    d = nb.conv(0, 48, (1, 7), 1, (0, 3), name="k1x7")
+    nb.conv(d, 40, (7, 1), 1, (3, 0), name="k7x1")
+    nb.conv(0, 64, 3, 2, 1, name="k3s2p1")
+    nb.conv(0, 24, 3, 3, 1, name="k3s3p1")
+    nb.conv(0, 16, 7, 2, 3, name="k7s2p3")
+    nb.conv(a, 56, 3, 1, 1, relu=False, name="chain")
+    nb.conv(a, 24, 1, 1, 0, name="k1")
+    nb.conv(0, 40, 2, 1, 0, name="k2s1p0")
+    nb.new_block()
+    m1 = nb.conv(a, 32, 3, 1, 1, name="m3")
+    m2 = nb.conv(a, 32, 1, 1, 0, name="m1")
+    m3 = nb.conv(a, 16, 5, 1, 2, name="m5")
+    nb.concat([m1, m2, m3], name="cat")
+    return nb.net
+
+
 # --------------------------------------------------------------------------------------------
 # Inception V3 (torchvision topology; Conv-Relu units, BN folded into bias)
 # --------------------------------------------------------------------------------------------
@@ -373,6 +397,7 @@ NETWORKS: Dict[str, Callable[..., NetSpec]] = {
     "fig2": fig2_block,
     "fig5": fig5_graph,
     "tiny_mixed": tiny_mixed_net,
+    "conv_zoo": conv_zoo_net,
     "inception_v3": inception_v3,
     "squeezenet": squeezenet,
     "nasnet_a_large": nasnet_a_large,
