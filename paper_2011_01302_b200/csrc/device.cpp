@@ -339,6 +339,7 @@ struct TileKnobs {
   int min_bn_small;   // narrowest N tile for small-M (<= 2 m-tiles) GEMMs
   int min_bn;         // narrowest N tile otherwise
   int one_wave;       // never refine past the target unit count (one wave of CTAs)
+  int simt_in_target; // count SIMT tiles toward the target
 };
 static TileKnobs tile_knobs() {
   static TileKnobs k = [] {
@@ -347,7 +348,7 @@ static TileKnobs tile_knobs() {
       return v ? atoi(v) : d;
     };
     return TileKnobs{env("IOS_TARGET_UNITS", 0), env("IOS_MIN_CPS", 4), env("IOS_MIN_BN_SMALL", 16),
-                     env("IOS_MIN_BN", 32), env("IOS_ONE_WAVE", 1)};
+                     env("IOS_MIN_BN", 32), env("IOS_ONE_WAVE", 1), env("IOS_SIMT_IN_TARGET", 0)};
   }();
   return k;
 }
@@ -379,7 +380,9 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
   // Fill the SMs: refine the problem with the most expensive tile (N halving first, then split-K)
   // until there are about as many units as the target.
   for (int it = 0; it < 256; ++it) {
-    int units = simt_tiles;
+    // SIMT tiles mostly run in another phase (a depthwise before its pointwise GEMM, pools beside
+    // short GEMMs), so by default the GEMM units alone are sized to one wave
+    int units = kn.simt_in_target ? simt_tiles : 0;
     for (GemmSpec* p : gs) units += p->mt * p->ntn * p->split;
     if (units >= target) break;
     GemmSpec* best = nullptr;
@@ -673,10 +676,13 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
         p.n_items = p.batch * p.Ho * ((p.Wo + p.dwq - 1) / p.dwq);
         p.items_per_tile = std::max(1, 128 / std::max(1, nvec));
       } else {
-        // about 4 vector items per epilogue thread so the stage spreads over many SMs
+        // about 2 vector items per epilogue thread so the stage spreads over many SMs
         p.n_items = p.batch * p.Ho * p.Wo;
         p.items_per_tile = std::max(1, 256 / std::max(1, nvec));
       }
+      // never more tiles than CTAs for one problem: a second wave doubles a latency-bound op
+      if (p.kind != PK_GAVGPOOL)
+        p.items_per_tile = std::max(p.items_per_tile, (p.n_items + d.num_sms - 1) / d.num_sms);
       p.n_tiles = (p.n_items + p.items_per_tile - 1) / p.items_per_tile;
       simt_tiles += p.n_tiles;
     }

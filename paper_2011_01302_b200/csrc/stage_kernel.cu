@@ -67,6 +67,9 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, uint64_t tmap, int c0,
       "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
       : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cnt(uint32_t a, uint32_t n) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(n) : "memory");
 }
@@ -684,7 +687,9 @@ __device__ __forceinline__ int find_problem(const int* sm_tile_begin, int n_prob
 template <int DT, bool SD>
 __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc sd) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip would make every
+  // derived pointer generic: generic loads wait behind outstanding global stores)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                       // kStages x 16 KB
   uint8_t* sB = smem + kStages * kAStageBytes;              // kStages x 32 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStageBytes);
@@ -766,6 +771,22 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Weight prefetch into L2: weights are never written by earlier stages, so
+  // before waiting for the previous grid every CTA asks L2 for its 1/grid share of each GEMM
+  // member's packed weights; the stage's weight stream then overlaps the previous stage's tail.
+#ifndef IOS_NO_PREFETCH
+  if (warp == kMmaWarp && sd.has_gemm) {
+    for (int q = lane; q < sd.n_problems; q += 32) {
+      const Problem& P = probs[q];
+      if (P.kind != PK_GEMM) continue;
+      const uint64_t total = (uint64_t)P.k_chunks * P.Npad8 * kChunkBytes;
+      const uint64_t share = ((total + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+      const uint64_t b0 = share * blockIdx.x, b1 = b0 + share < total ? b0 + share : total;
+      for (uint64_t o = b0; o < b1; o += 32768)
+        prefetch_l2(reinterpret_cast<const uint8_t*>(P.wts) + o, (uint32_t)(b1 - o < 32768 ? b1 - o : 32768));
+    }
+  }
+#endif
   // programmatic dependent launch: the prologue above overlapped the previous stage's tail; from
   // here on we read activations (and counters) the previous grid may still be writing
   if (tid == 0) IOS_TRACE(11);   // before waiting for the previous grid
