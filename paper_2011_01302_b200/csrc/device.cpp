@@ -860,6 +860,37 @@ void check_err(DeviceState& d) {
 
 }  // namespace
 
+namespace {
+// A stream-captured CUDA graph (owned; destroyed with the object).
+struct GraphExec {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  GraphExec() = default;
+  GraphExec(const GraphExec&) = delete;
+  GraphExec(GraphExec&& o) noexcept : graph(o.graph), exec(o.exec) { o.graph = nullptr; o.exec = nullptr; }
+  ~GraphExec() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+template <class F>
+GraphExec capture(DeviceState& d, F&& body) {
+  GraphExec g;
+  IOS_CHECK_CUDA(cudaStreamBeginCapture(d.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(d.stream, &junk);
+    if (junk) cudaGraphDestroy(junk);
+    throw;
+  }
+  IOS_CHECK_CUDA(cudaStreamEndCapture(d.stream, &g.graph));
+  IOS_CHECK_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+  return g;
+}
+}  // namespace
+
 double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const ios_profile_opts* opts) {
   ensure_device(g);
   DeviceState& d = *g.dev;
@@ -899,11 +930,16 @@ double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const 
   if (!p->empty) {
     if (flush && !d.l2buf) d.l2buf = dmalloc(d, (size_t)d.l2bytes);
     for (int i = 0; i < warmup; ++i) launch_plan(p, d.stream);
+    // the `reps` back-to-back launches are one CUDA graph, the launch mechanism ios_run uses
+    // (the DP must measure stages the way they run)
+    GraphExec rep = capture(d, [&] {
+      for (int i = 0; i < reps; ++i) launch_plan(p, d.stream);
+    });
     std::vector<double> t;
     for (int tr = 0; tr < trials; ++tr) {
       if (flush) IOS_CHECK_CUDA(launch_l2_flush(d.l2buf, d.l2bytes, d.stream));
       IOS_CHECK_CUDA(cudaEventRecord(d.ev0, d.stream));
-      for (int i = 0; i < reps; ++i) launch_plan(p, d.stream);
+      IOS_CHECK_CUDA(cudaGraphLaunch(rep.exec, d.stream));
       IOS_CHECK_CUDA(cudaEventRecord(d.ev1, d.stream));
       IOS_CHECK_CUDA(cudaEventSynchronize(d.ev1));
       float e = 0;
@@ -961,15 +997,22 @@ void measure_stages(Graph& g, int bpos, const std::vector<std::pair<uint64_t, in
         g.latency_cache[std::make_tuple(sig, mask, t)] = kInf;
       }
     }
-    for (auto* p : plans)
-      if (p) launch_plan(p, d.stream);   // warm-up
-    for (int tr = 0; tr < kTrials; ++tr)
-      for (size_t i = 0; i < plans.size(); ++i) {
-        if (!plans[i] || plans[i]->empty) continue;
-        IOS_CHECK_CUDA(cudaEventRecord(event(2 * (tr * kBatch + i)), d.stream));
-        for (int r = 0; r < kReps; ++r) launch_plan(plans[i], d.stream);
-        IOS_CHECK_CUDA(cudaEventRecord(event(2 * (tr * kBatch + i) + 1), d.stream));
-      }
+    for (size_t i = 0; i < 2 * kTrials * kBatch; ++i) event(i);
+    // warm-up + all trials of the batch as ONE CUDA graph (event-record nodes around each plan's
+    // launches): stages are timed under the launch mechanism ios_run uses
+    GraphExec batch = capture(d, [&] {
+      for (auto* p : plans)
+        if (p) launch_plan(p, d.stream);   // warm-up
+      for (int tr = 0; tr < kTrials; ++tr)
+        for (size_t i = 0; i < plans.size(); ++i) {
+          if (!plans[i] || plans[i]->empty) continue;
+          // External: a captured record becomes a real event-record node (not a capture join)
+          IOS_CHECK_CUDA(cudaEventRecordWithFlags(ev[2 * (tr * kBatch + i)], d.stream, cudaEventRecordExternal));
+          for (int r = 0; r < kReps; ++r) launch_plan(plans[i], d.stream);
+          IOS_CHECK_CUDA(cudaEventRecordWithFlags(ev[2 * (tr * kBatch + i) + 1], d.stream, cudaEventRecordExternal));
+        }
+    });
+    IOS_CHECK_CUDA(cudaGraphLaunch(batch.exec, d.stream));
     IOS_CHECK_CUDA(cudaStreamSynchronize(d.stream));
     check_err(d);
     for (size_t i = 0; i < plans.size(); ++i) {

@@ -76,7 +76,7 @@ struct Problem {
   int32_t Ho, Wo;
   int32_t in_begin, n_in;           // views[in_begin .. in_begin + n_in)
   View out;                         // SIMT output / GEMM: unused (segments)
-  uint64_t wts;                     // GEMM: packed weights; DWCONV: fp32 [C][kh*kw]
+  uint64_t wts;                     // GEMM: packed weights; DWCONV: fp32 tap-major [kh*kw][C]
   uint64_t bias;                    // fp32 [N padded]
   uint64_t add_w;                   // fp32 [n_in] or 0
   // GEMM geometry
@@ -85,7 +85,8 @@ struct Problem {
   int32_t split, chunks_per_split;
   int32_t Npad8;                    // packed weight rows (multiple of 8)
   int32_t seg_begin, n_seg;
-  uint64_t workspace;               // split-K partials [out tiles][split][kBM][BN] fp32
+  uint64_t workspace;               // split-K fp32 sums, per output tile [kBM][BN] (swap-AB:
+                                    // channel-major [128][BN]); re-zeroed by the finalize
   int32_t tilectr_idx;              // split-K arrival counters base
   int32_t signal;                   // 1: a later member of the stage waits on done_idx
   FastDiv fd_howo, fd_wo, fd_split, fd_ntn, fd_cin, fd_kw;   // divisors of the tile / im2col decode
@@ -110,13 +111,14 @@ struct StageDesc {
   uint64_t problems;                // Problem[n_problems]
   uint64_t views;                   // View[]
   uint64_t segs;                    // Segment[]
-  uint64_t counters;                // int32[n_counters]; [0] = CTA exit counter
+  uint64_t counters;                // int32[n_counters]; [0] = launch epoch (see uses_counters)
   uint64_t err;                     // int32 error flag (dependency-wait timeout)
   uint64_t trace;                   // optional uint64 [grid][16] timeline (0 = off)
   int32_t n_problems, n_tiles, n_counters, has_gemm;
   int32_t blob_bytes;               // problems | views | segments, contiguous from `problems`
   int32_t views_off, segs_off;
-  int32_t uses_counters;            // any in-stage dependency or split-K: reset counters at exit
+  int32_t uses_counters;            // any in-stage dependency or split-K: counters[0] is the launch
+                                    // epoch, the others grow monotonically (targets epoch-relative)
 };
 
 }  // namespace ios

@@ -285,10 +285,13 @@ __device__ __forceinline__ void store_elem(const View& vw, int dtype, int64_t pi
 }
 
 // ------------------------------------------------------------------------------ dependency waits
-__device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* err) {
+// Counters are never reset: every launch adds the same amounts, and launch number `ep` (the epoch,
+// derived at kernel start) turns the per-launch targets into absolute ones: wait until
+// counter >= (ep + 1) * target (int arithmetic; wraps only after ~10^7 launches of one plan).
+__device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* err, int ep) {
   for (int d = 0; d < P.n_deps; ++d) {
     const int* c = counters + P.dep_idx[d];
-    const int target = P.dep_target[d];
+    const int target = (ep + 1) * P.dep_target[d];
     long long t0 = clock64();
     while (ld_acquire(c) < target) {
       __nanosleep(64);
@@ -303,10 +306,11 @@ __device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* 
 // split-K rendezvous: every split of an output tile arrives after its reductions, then waits for
 // all `n` (the splits of one tile run on distinct, co-resident CTAs; a tile's splits only wait for
 // tiles with higher indices, which the CTAs reach after finishing lower ones: no cycle)
-__device__ __forceinline__ void split_rendezvous(int* ctr, int n, int* err) {
+__device__ __forceinline__ void split_rendezvous(int* ctr, int n, int* err, int ep) {
   atom_acqrel_add(ctr, 1);
+  const int target = (ep + 1) * n;
   long long t0 = clock64();
-  while (ld_acquire(ctr) < n) {
+  while (ld_acquire(ctr) < target) {
     __nanosleep(32);
     if (clock64() - t0 > (long long)8000000000LL) {
       atomicExch(err, 1);
@@ -375,10 +379,13 @@ __device__ __noinline__ void win_tile(const Problem& P, const View* views, int t
     for (int u = 0; u < QW; ++u)
 #pragma unroll
       for (int e = 0; e < NV; ++e) acc[u][e] = neutral;
+    // rows fully unrolled with a validity predicate (no early `continue`), so the loads of
+    // several window rows can be in flight together
+#pragma unroll
     for (int i = 0; i < K; ++i) {
       const int ih = hs + i;
-      if ((unsigned)ih >= (unsigned)in.H) continue;
-      const int64_t rowpix = ((int64_t)n * in.H + ih) * in.W + ws;
+      const bool rok = (unsigned)ih < (unsigned)in.H;
+      const int64_t rowpix = ((int64_t)n * in.H + (rok ? ih : 0)) * in.W + ws;
       float xr[SPAN][NV];
       if (KIND == 0 && nin > 1) {
 #pragma unroll
@@ -390,7 +397,7 @@ __device__ __noinline__ void win_tile(const Problem& P, const View* views, int t
           const float w = awv[s];
 #pragma unroll
           for (int t = 0; t < SPAN; ++t) {
-            if ((unsigned)(ws + t) < (unsigned)in.W) {
+            if (rok && (unsigned)(ws + t) < (unsigned)in.W) {
               float x[NV];
               ld16<DT>(vs, rowpix + t, c, x);
 #pragma unroll
@@ -401,7 +408,7 @@ __device__ __noinline__ void win_tile(const Problem& P, const View* views, int t
       } else {
 #pragma unroll
         for (int t = 0; t < SPAN; ++t) {
-          if ((unsigned)(ws + t) < (unsigned)in.W) {
+          if (rok && (unsigned)(ws + t) < (unsigned)in.W) {
             ld16<DT>(in, rowpix + t, c, xr[t]);
           } else {
 #pragma unroll
@@ -791,7 +798,12 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   // here on we read activations (and counters) the previous grid may still be writing
   if (tid == 0) IOS_TRACE(11);   // before waiting for the previous grid
   pdl_wait();
+  // launch epoch: every CTA of a launch adds 1 to counters[0] exactly once, before releasing the
+  // next launch (launch_dependents), so old / grid is this launch's number for every CTA
+  if (sd.uses_counters && tid == 0) *flag = atomicAdd(counters, 1) / (int)gridDim.x;
   pdl_launch_dependents();
+  named_bar(4, kThreads);
+  const int ep = sd.uses_counters ? *flag : 0;
   if (tid == 0) IOS_TRACE(1);
 
   if (!sd.has_gemm) {
@@ -800,7 +812,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     for (int t = blockIdx.x; t < sd.n_tiles; t += gridDim.x) {
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
-      if (tid == 0) wait_deps(P, counters, err);
+      if (tid == 0) wait_deps(P, counters, err, ep);
       named_bar(3, kThreads);
 #ifndef IOS_NO_SIMT
       simt_tile<DT>(P, views, t - P.tile_begin, tid, kThreads);
@@ -825,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const Problem& P = probs[hint];
       if (P.kind != PK_GEMM) continue;
       if (P.n_deps) {
-        if (ptid == 0) wait_deps(P, counters, err);
+        if (ptid == 0) wait_deps(P, counters, err, ep);
         named_bar(1, 128);
       }
       const int local = t - P.tile_begin;
@@ -1088,7 +1100,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
       if (P.kind != PK_GEMM) {
-        if (etid == 0) wait_deps(P, counters, err);
+        if (etid == 0) wait_deps(P, counters, err, ep);
         named_bar(2, 128);
 #ifndef IOS_NO_SIMT
         simt_tile<DT>(P, views, t - P.tile_begin, etid, 128);
@@ -1227,7 +1239,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty[acc]));
           named_bar(2, 128);
-          if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err);
+          if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep);
           named_bar(2, 128);
           // distributed finalize: split s owns pixel quads [s*np4/S, (s+1)*np4/S) of the tile; each
           // thread reads its channel's quads (float4, 8 in flight), re-zeroes them, and emits them
@@ -1445,7 +1457,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         tc_fence_before();
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
         named_bar(2, 128);
-        if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err);
+        if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep);
         named_bar(2, 128);
         {
           // distributed finalize (see the swap-AB path): split s owns tile rows
@@ -1524,16 +1536,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols) : "memory");
   }
   if (tid == 0) {
-    IOS_TRACE(7);
-    if (sd.uses_counters) {
-      // the last CTA out resets the stage's counters for the next launch (graph-replay safe)
-      const int old = atom_acqrel_add(counters, 1);
-      if (old == (int)gridDim.x - 1) {
-        for (int i = 1; i < sd.n_counters; ++i) counters[i] = 0;
-        __threadfence();
-        counters[0] = 0;
-      }
-    }
+    IOS_TRACE(7);   // counters are epoch-relative: nothing to reset at exit
     IOS_TRACE(8);
   }
 #undef IOS_TRACE
