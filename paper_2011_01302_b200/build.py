@@ -28,13 +28,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
     procs = []
-    for src in SOURCES:
-        obj = os.path.join(HERE, "build", src + ".o")
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        if src.endswith(".cu"):
-            cmd += ["-Xptxas", "-v"] if verbose else []
-        else:
-            cmd += ["-x", "cu"] if False else []
+    # the stage kernel's six (dtype, smem-descriptor) instantiations are separate units so they
+    # compile in parallel (stage_kernel.cu, IOS_INST_DT / IOS_INST_SD)
+    units = [(src, []) for src in SOURCES]
+    units += [("stage_kernel.cu", [f"-DIOS_INST_DT={dt}", f"-DIOS_INST_SD={sdv}"]) for dt in range(3) for sdv in range(2)]
+    for src, defs in units:
+        tag = "".join(d.split("=")[1] for d in defs)
+        obj = os.path.join(HERE, "build", src + (f".inst{tag}" if tag else "") + ".o")
+        cmd = [NVCC, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", obj]
+        if src.endswith(".cu") and verbose:
+            cmd += ["-Xptxas", "-v"]
         procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
     failed = False

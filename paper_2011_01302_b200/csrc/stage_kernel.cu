@@ -1542,6 +1542,22 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #undef IOS_TRACE
 }
 
+#ifdef IOS_INST_DT
+#define IOS_LAUNCHER_DEF2(dt, sdv) IOS_LAUNCHER_DECL(dt, sdv)
+#define IOS_LAUNCHER_DECL(dt, sdv) cudaError_t launch_stage_inst_##dt##_##sdv(cudaLaunchConfig_t& cfg, const StageDesc& sd)
+IOS_LAUNCHER_DEF2(IOS_INST_DT, IOS_INST_SD) {
+  static bool attr_done = false;
+  auto k = ios_stage_kernel<IOS_INST_DT, (IOS_INST_SD != 0)>;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  return cudaLaunchKernelEx(&cfg, k, sd);
+}
+
+}  // namespace ios
+#else
 // ------------------------------------------------------------------------ boundary layout kernels
 // NCHW fp32 (caller) -> NHWC padded (internal); rounds to the storage precision (Z14).
 __global__ void nchw_to_nhwc_kernel(const float* __restrict__ in, View out, int dtype, int N, int C) {
@@ -1575,18 +1591,14 @@ __global__ void l2_flush_kernel(int4* buf, int64_t n) {
 }
 
 // ------------------------------------------------------------------------------ host launchers
+// The six (DT, SD) instantiations of the stage kernel are compiled as separate translation units
+// (build.py passes -DIOS_INST_DT=<dt> -DIOS_INST_SD=<0|1>; nvcc runs them in parallel). Each unit
+// exports one plain host launcher; launch_stage (host unit) dispatches to them.
+#define IOS_LAUNCHER_DECL(dt, sdv) cudaError_t launch_stage_inst_##dt##_##sdv(cudaLaunchConfig_t& cfg, const StageDesc& sd)
+IOS_LAUNCHER_DECL(0, 0); IOS_LAUNCHER_DECL(0, 1); IOS_LAUNCHER_DECL(1, 0);
+IOS_LAUNCHER_DECL(1, 1); IOS_LAUNCHER_DECL(2, 0); IOS_LAUNCHER_DECL(2, 1);
+
 cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    const void* ks[6] = {(const void*)ios_stage_kernel<ET_F32, true>, (const void*)ios_stage_kernel<ET_F32, false>,
-                         (const void*)ios_stage_kernel<ET_BF16, true>, (const void*)ios_stage_kernel<ET_BF16, false>,
-                         (const void*)ios_stage_kernel<ET_F32X, true>, (const void*)ios_stage_kernel<ET_F32X, false>};
-    cudaError_t e = cudaSuccess;
-    for (int i = 0; i < 6 && e == cudaSuccess; ++i)
-      e = cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -1598,14 +1610,9 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool smem_desc = sd.blob_bytes <= kDescBytes;
-  if (dtype == ET_BF16)
-    return smem_desc ? cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_BF16, true>, sd)
-                     : cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_BF16, false>, sd);
-  if (dtype == ET_F32X)
-    return smem_desc ? cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32X, true>, sd)
-                     : cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32X, false>, sd);
-  return smem_desc ? cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32, true>, sd)
-                   : cudaLaunchKernelEx(&cfg, ios_stage_kernel<ET_F32, false>, sd);
+  if (dtype == ET_BF16) return smem_desc ? launch_stage_inst_1_1(cfg, sd) : launch_stage_inst_1_0(cfg, sd);
+  if (dtype == ET_F32X) return smem_desc ? launch_stage_inst_2_1(cfg, sd) : launch_stage_inst_2_0(cfg, sd);
+  return smem_desc ? launch_stage_inst_0_1(cfg, sd) : launch_stage_inst_0_0(cfg, sd);
 }
 
 cudaError_t launch_nchw_to_nhwc(const float* in, const View& out, int dtype, int N, int C, cudaStream_t st) {
@@ -1629,3 +1636,4 @@ cudaError_t launch_l2_flush(void* buf, int64_t bytes, cudaStream_t st) {
 }
 
 }  // namespace ios
+#endif  // !IOS_INST_DT
