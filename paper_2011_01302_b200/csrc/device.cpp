@@ -30,6 +30,7 @@ struct OpDev {
   int wpack_n8 = 0;           // packed rows (multiple of 8)
   float* bias = nullptr;      // fp32, zero padded
   float* dw = nullptr;        // sepconv depthwise weights fp32, tap-major [kh*kw][Cp_in]
+  float* dwc = nullptr;       // the same, chunk-major [Cp_in / elems][kh*kw][elems] (fused halo path)
   float* add_w = nullptr;     // add / sepconv aggregation weights
   View dw_out{};              // sepconv depthwise scratch (NHWC, Cp_in channels)
   int tt = 0, kblk = 0;       // weights packed for the tap-TMA im2col path (K = taps x kblk blocks)
@@ -173,6 +174,27 @@ TTGeom tt_geometry(int batch, int Ho, int Wo, int sh, int sw) {
   return best;
 }
 
+// Fused Relu-SepConv patch tiles: at most 16 quads (QW adjacent columns) per tile, so each of the
+// 128 producer threads computes ONE (quad, 16 B piece) item per K chunk: the depthwise half is
+// latency-bound (dependent load rounds per item), so parallelism across CTAs beats M-tile fill
+// (the MMA is idle most of the time anyway). Fewest tiles wins.
+TTGeom fdw_geometry(int batch, int Ho, int Wo, int qw) {
+  constexpr int kQuads = 16;
+  TTGeom best;
+  for (int wt = std::min(Wo, kQuads * qw); wt >= 1; --wt) {
+    const int qpr = (wt + qw - 1) / qw;             // quads per patch row
+    const int r = std::max(1, std::min(Ho, kQuads / qpr));
+    const int tn = (r == Ho && wt == Wo) ? std::max(1, std::min(batch, kQuads / (qpr * Ho))) : 1;
+    const int th = (Ho + r - 1) / r, tw = (Wo + wt - 1) / wt;
+    const int tiles = ((batch + tn - 1) / tn) * th * tw;
+    if (best.tiles == 0 || tiles < best.tiles) {
+      best.tN = tn; best.tR = r; best.tWt = wt;
+      best.tiles_h = th; best.tiles_w = tw; best.tiles = tiles;
+    }
+  }
+  return best;
+}
+
 // Tap-TMA im2col eligibility: returns the number of 128 B channel blocks per tap (0 = use the
 // cp.async gather or the 2D TMA path). Pre-ReLU convs need the gather (the ReLU is applied on the
 // way to smem); 1x1/s1/unpadded convs take the plain 2D TMA; narrow inputs would pad K too much;
@@ -294,6 +316,13 @@ void ensure_device(Graph& g) {
       for (int ch = 0; ch < c; ++ch)
         for (int t = 0; t < kk; ++t) dw[(size_t)t * cp + ch] = o.weight[(size_t)ch * kk + t];
       e.dw = upload(d, dw);
+      {
+        const int el = kChunkBytes / g.esize(), nch = (cp + el - 1) / el;
+        std::vector<float> dwc((size_t)nch * kk * el, 0.0f);
+        for (int ch = 0; ch < c; ++ch)
+          for (int t = 0; t < kk; ++t) dwc[((size_t)(ch / el) * kk + t) * el + ch % el] = o.weight[(size_t)ch * kk + t];
+        e.dwc = upload(d, dwc);
+      }
       const float* PW = o.weight.data() + (size_t)c * kk;
       e.wpack = pack_gemm(d, o.Cp, cp, wdt, [&](int nn, int k) -> float {
         return (nn < o.cout && k < c) ? PW[(size_t)nn * c + k] : 0.0f;
@@ -314,7 +343,56 @@ struct GemmSpec {
   int swap;   // swap-AB: weights are the 128-row MMA operand, the (<= 128) pixels are N
   int max_bn = kMaxBN;
   int tt_tiles = 0;   // tap-TMA: number of patch M tiles (0 = dense 128-pixel tiles)
+  int fdw = 0;        // fused Relu-SepConv: split K down to one chunk, never narrow N (each N tile
+                      // would recompute the depthwise half)
+  double chunk_cost = 1.0;   // relative cost of one K chunk (fused depthwise chunks are compute)
 };
+
+// Fused Relu-SepConv eligibility: square window k in {3, 5, 7}, stride 1-2, at most
+// 8 aggregated inputs, tcgen05 math modes (FP32-SIMT keeps the two-problem form)
+bool fuse_dw_ok(const Graph& g, const Op& o) {
+  static const bool on = [] {
+    const char* v = getenv("IOS_FUSE_DW");
+    return v ? atoi(v) != 0 : true;
+  }();
+  if (!on || g.math == IOS_MATH_FP32_SIMT) return false;
+  if (o.kh != o.kw || o.sh != o.sw || o.ph != o.pw) return false;
+  if (!(o.kh == 3 || o.kh == 5 || o.kh == 7) || !(o.sh == 1 || o.sh == 2)) return false;
+  if (o.inputs.size() > 8) return false;
+  for (int u : o.inputs)
+    if (g.ops[u].Cp != g.ops[o.inputs[0]].Cp) return false;
+  // multi-input units (RandWire aggregation) have no halo path: their register-window form is
+  // slower than the two-problem form, so they stay unfused unless IOS_FUSE_DW=2
+  if (o.inputs.size() > 1 && !(getenv("IOS_FUSE_DW") && atoi(getenv("IOS_FUSE_DW")) >= 2)) return false;
+  return true;
+}
+
+// Halo-path patch tiles (single-input fused Relu-SepConv): the tile's input window
+// ((tWt-1)s+k) x ((tR-1)s+k) pixels x 128 B must fit kHaloBytes, at most 32 quads (2 items per
+// producer thread per chunk) and 128 pixels; most output pixels per tile, then fewest tiles.
+TTGeom halo_geometry(int batch, int Ho, int Wo, int k, int s, int qw) {
+  TTGeom best;
+  int best_px = 0;
+  for (int wt = std::min(Wo, kBM); wt >= 1; --wt) {
+    const int ws = (wt - 1) * s + k;
+    if (ws > 256) continue;
+    const int qpr = (wt + qw - 1) / qw;
+    for (int r = std::min(Ho, kBM / wt); r >= 1; --r) {
+      const int hs = (r - 1) * s + k;
+      if (hs > 256 || ws * hs * kChunkBytes > kHaloBytes || qpr * r > 32) continue;
+      const int th = (Ho + r - 1) / r, tw = (Wo + wt - 1) / wt;
+      const int tiles = batch * th * tw;
+      const int px = r * wt;
+      if (best.tiles == 0 || tiles < best.tiles || (tiles == best.tiles && px > best_px)) {
+        best.tN = 1; best.tR = r; best.tWt = wt;
+        best.tiles_h = th; best.tiles_w = tw; best.tiles = tiles;
+        best_px = px;
+      }
+      break;   // the largest r that fits is best for this wt
+    }
+  }
+  return best;
+}
 
 bool tap_tma_enabled() {
   static const bool on = [] {
@@ -390,10 +468,11 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
     for (GemmSpec* p : gs) {
       // small-M GEMMs are weight-bound: narrow N tiles first (A is small and L2-resident), then split K
       const int min_bn = p->mt <= 2 ? kn.min_bn_small : kn.min_bn;
-      const bool can_n = !p->swap && p->BN >= 2 * min_bn;
-      const bool can_k = p->cps >= 2 * kn.min_cps && p->split < 32;
+      const int min_cps = p->fdw ? 1 : kn.min_cps;
+      const bool can_n = !p->swap && !p->fdw && p->BN >= 2 * min_bn;
+      const bool can_k = p->cps >= 2 * min_cps && p->split < 32;
       if (!can_n && !can_k) continue;
-      const double c = p->cps * (1.0 + p->BN / 256.0);
+      const double c = p->cps * p->chunk_cost * (1.0 + p->BN / 256.0);
       if (c > best_cost) {
         best_cost = c;
         best = p;
@@ -404,7 +483,8 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
     // replaced by the largest split-K that still fits, or refinement stops
     const int cur = best->mt * best->ntn * best->split;
     const int others = units - cur;
-    const bool can_n = !best->swap && best->BN >= 2 * (best->mt <= 2 ? kn.min_bn_small : kn.min_bn);
+    const bool can_n = !best->swap && !best->fdw && best->BN >= 2 * (best->mt <= 2 ? kn.min_bn_small : kn.min_bn);
+    const int best_min_cps = best->fdw ? 1 : kn.min_cps;
     if (can_n && (!kn.one_wave || others + 2 * cur <= target)) {
       best->BN = round_up(best->BN / 2, 16);
       best->ntn = (best->N16 + best->BN - 1) / best->BN;
@@ -412,7 +492,7 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       int want = best->split * 2;
       const int room = (target - others) / (best->mt * best->ntn);
       if (kn.one_wave && want > room) want = room;
-      if (want <= best->split || (best->kch + want - 1) / want < kn.min_cps) break;
+      if (want <= best->split || (best->kch + want - 1) / want < best_min_cps) break;
       best->cps = (best->kch + want - 1) / want;
       best->split = (best->kch + best->cps - 1) / best->cps;
     }
@@ -619,6 +699,41 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
             break;
           }
           case IOS_OP_SEPCONV: {
+            if (fuse_dw_ok(g, o)) {
+              // fused Relu-SepConv: ONE GEMM problem whose producer computes the
+              // depthwise half into the A operand; M tiles are output patches (epilogue mapping of
+              // tap-TMA tiles), K = the input channels
+              const int u0 = o.inputs[0];
+              const int pi = b.gemm(-1, d.od[u0].out, e.wpack, e.wpack_n8, e.bias, o.Cp, 1, 1, 1, 1, 0, 0, o.H, o.W, 0);
+              for (size_t k = 1; k < o.inputs.size(); ++k) b.views.push_back(d.od[o.inputs[k]].out);
+              Problem& p = b.probs[pi];
+              p.n_in = (int)o.inputs.size();
+              p.fdw = 1;
+              p.dk = o.kh; p.ds = o.sh; p.dp = o.ph;
+              p.dH = g.ops[u0].H; p.dW = g.ops[u0].W;
+              p.dww = (uint64_t)e.dw;
+              p.add_w = (uint64_t)e.add_w;
+              const int qw = g.math == IOS_MATH_BF16 ? 2 : 4;
+              const bool halo = o.inputs.size() == 1;
+              const TTGeom tg = halo ? halo_geometry(g.batch, o.H, o.W, o.kh, o.sh, qw) : fdw_geometry(g.batch, o.H, o.W, qw);
+              if (halo) {
+                p.hws = (tg.tWt - 1) * o.sw + o.kw;
+                p.hhs = (tg.tR - 1) * o.sh + o.kh;
+                p.dwc = (uint64_t)e.dwc;
+              }
+              p.tt = 1;
+              p.tN = tg.tN; p.tR = tg.tR; p.tWt = tg.tWt;
+              p.tiles_h = tg.tiles_h; p.tiles_w = tg.tiles_w;
+              GemmSpec& sp = b.specs[pi];
+              sp.tt_tiles = tg.tiles;
+              sp.swap = 0;
+              sp.fdw = 1;
+              sp.chunk_cost = 1.0 + o.kh * o.kw / 4.0;
+              b.seg(pi, 0, o.Cp, e.out, (o.flags & IOS_F_RELU_POST) ? 1 : 0);
+              b.add_deps(pi, deps);
+              b.op_probs[v] = {pi};
+              break;
+            }
             Op dwop = o;
             const int pd = b.simt(PK_DWCONV, dwop, o.inputs, e.dw_out, o.flags);
             b.probs[pd].wts = (uint64_t)e.dw;
@@ -704,14 +819,14 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       p.fd_cin = make_fastdiv((uint32_t)in.C);
       p.fd_kw = make_fastdiv((uint32_t)p.kw);
       if (p.tt) {
-        p.fd_kblk = make_fastdiv((uint32_t)p.kblk);
+        p.fd_kblk = make_fastdiv((uint32_t)std::max(1, p.kblk));
         p.fd_thw = make_fastdiv((uint32_t)(p.tR * p.tWt));
         p.fd_tw = make_fastdiv((uint32_t)p.tWt);
         p.fd_tilw = make_fastdiv((uint32_t)p.tiles_w);
         p.fd_tilh = make_fastdiv((uint32_t)p.tiles_h);
       }
       // A via TMA when it is a plain [M, C] matrix: 1x1, stride 1, no padding, no pre-ReLU
-      p.a_tma = (g.math != IOS_MATH_FP32_SIMT && p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 && p.pw == 0 &&
+      p.a_tma = (g.math != IOS_MATH_FP32_SIMT && !p.fdw && p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 && p.pw == 0 &&
                  !(p.flags & IOS_F_RELU_PRE)) ? 1 : 0;
       p.swap_ab = s.swap;
       p.BN = s.BN;
@@ -722,7 +837,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       p.n_tiles = s.mt * s.ntn * s.split;
       if (p.split > 1) {
         p.workspace = ws_bytes;   // offset for now
-        ws_bytes += (size_t)s.mt * s.ntn * kBM * s.BN * sizeof(float);   // zeroed fp32 accumulators (red.add)
+        ws_bytes += (size_t)s.mt * s.ntn * s.split * kBM * s.BN * sizeof(float);   // one fp32 partial slab per split
         p.tilectr_idx = n_tilectr;
         n_tilectr += s.mt * s.ntn;
       }
@@ -766,12 +881,24 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
           g.math == IOS_MATH_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
       const cuuint32_t elems = (cuuint32_t)(kChunkBytes / g.esize());
       for (Problem& p : b.probs) {
-        if (p.kind != PK_GEMM || !(p.a_tma || p.tt)) continue;
+        if (p.kind != PK_GEMM || (p.fdw && !p.hws) || !(p.a_tma || p.tt)) continue;
         const View& in = b.views[p.in_begin];
         CUtensorMap tm;
         void* base = reinterpret_cast<char*>(in.ptr) + (size_t)in.coff * g.esize();
         CUresult r;
-        if (p.a_tma) {
+        if (p.hws) {
+          // fused Relu-SepConv halo: NHWC input {C, W, H, N}, box = one 128 B channel chunk of an
+          // hhs x hws input window, dense (no swizzle); padding = out-of-bounds zeros
+          const cuuint64_t dims[4] = {(cuuint64_t)in.C, (cuuint64_t)in.W, (cuuint64_t)in.H, (cuuint64_t)p.batch};
+          const cuuint64_t rs = (cuuint64_t)in.cstride * g.esize();
+          const cuuint64_t strides[3] = {rs, rs * in.W, rs * in.W * in.H};
+          const cuuint32_t box[4] = {elems, (cuuint32_t)p.hws, (cuuint32_t)p.hhs, 1};
+          const cuuint32_t estr[4] = {1, 1, 1, 1};
+          r = encode_tiled()(&tm, tdt, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (r != CUDA_SUCCESS) IOS_FAIL(IOS_ERR_CUDA, "halo tensor map rejected by the driver");
+        } else if (p.a_tma) {
           // [M, C] matrix: 128 rows x 128 B per box
           const cuuint64_t dims[2] = {(cuuint64_t)in.C, (cuuint64_t)p.M};
           const cuuint64_t strides[1] = {(cuuint64_t)in.cstride * g.esize()};
@@ -803,7 +930,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       if (!maps.empty()) {
         void* mp = upload(d, maps, 0, &plan->allocs);
         for (Problem& p : b.probs)
-          if (p.kind == PK_GEMM && (p.a_tma || p.tt)) p.tmap_a = (uint64_t)mp + p.tmap_a * sizeof(CUtensorMap);
+          if (p.kind == PK_GEMM && (!p.fdw || p.hws) && (p.a_tma || p.tt)) p.tmap_a = (uint64_t)mp + p.tmap_a * sizeof(CUtensorMap);
       }
       std::memcpy(blob.data(), b.probs.data(), pb);
       plan->dmem = upload(d, blob, 0, &plan->allocs);
@@ -822,6 +949,9 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       sd.segs_off = (int)(pb + vb);
       sd.uses_counters = 0;
       for (Problem& p : b.probs) sd.uses_counters |= (p.signal || (p.kind == PK_GEMM && p.split > 1)) ? 1 : 0;
+      sd.ring_slots = kStages;
+      for (Problem& p : b.probs)
+        if (p.kind == PK_GEMM && p.hws) sd.ring_slots = kStages - 1;
       sd.has_gemm = 0;
       for (Problem& p : b.probs) sd.has_gemm |= p.kind == PK_GEMM;
       plan->grid = std::min(tiles, d.num_sms);

@@ -85,8 +85,8 @@ struct Problem {
   int32_t split, chunks_per_split;
   int32_t Npad8;                    // packed weight rows (multiple of 8)
   int32_t seg_begin, n_seg;
-  uint64_t workspace;               // split-K fp32 sums, per output tile [kBM][BN] (swap-AB:
-                                    // channel-major [128][BN]); re-zeroed by the finalize
+  uint64_t workspace;               // split-K fp32 partials, per output tile [split][kBM][BN] (swap-AB:
+                                    // channel-major [split][128][BN]); summed in split order
   int32_t tilectr_idx;              // split-K arrival counters base
   int32_t signal;                   // 1: a later member of the stage waits on done_idx
   FastDiv fd_howo, fd_wo, fd_split, fd_ntn, fd_cin, fd_kw;   // divisors of the tile / im2col decode
@@ -105,7 +105,22 @@ struct Problem {
   int32_t kblk, tN, tR, tWt, tiles_h, tiles_w;
   FastDiv fd_kblk, fd_thw, fd_tw, fd_tilw, fd_tilh;
   uint64_t tmap_a;                  // global address of its CUtensorMap (2D / 4D tiled, 128B swizzle)
+  // fused Relu-SepConv: the producer warps compute the depthwise half of the unit
+  // straight into the A operand of its pointwise GEMM (patch M tiles as with tap TMA, K = the
+  // input channels); inputs [in_begin, in_begin + n_in) are aggregated with add_w first
+  int32_t fdw;                      // 1: fused depthwise A producer
+  int32_t dk, ds, dp;               // depthwise window (square k in {3, 5, 7}), stride, padding
+  int32_t dH, dW;                   // depthwise input spatial size
+  uint64_t dww;                     // fp32 tap-major [k*k][Cin_p] depthwise weights
+  uint64_t dwc;                     // fp32 chunk-major [k_chunks][k*k][elems per 128 B chunk] (halo path)
+  int32_t hws, hhs;                 // halo path: input window of one patch tile = hhs rows x hws columns,
+                                    // staged by ONE 4D tensor TMA (tmap_a) per K chunk, OOB = padding zeros
 };
+
+// halo path (single-input fused Relu-SepConv): the stage runs its smem ring with 3 slots; slot 3's
+// B region holds the input window of the chunk, slot 3's A region the chunk's depthwise weights
+constexpr int kHaloBytes = kBStageBytes;          // 32 KB: <= 256 pixels x 128 B
+constexpr int kHaloWBytes = kAStageBytes;         // 16 KB: k*k x 128 B (fp32) / 256 B (bf16 chunk)
 
 struct StageDesc {
   uint64_t problems;                // Problem[n_problems]
@@ -119,6 +134,8 @@ struct StageDesc {
   int32_t views_off, segs_off;
   int32_t uses_counters;            // any in-stage dependency or split-K: counters[0] is the launch
                                     // epoch, the others grow monotonically (targets epoch-relative)
+  int32_t ring_slots;               // smem ring depth this launch: kStages, or kStages - 1 when a halo
+                                    // problem borrows the last slot
 };
 
 }  // namespace ios

@@ -392,6 +392,7 @@ __device__ __noinline__ void win_tile(const Problem& P, const View* views, int t
         for (int t = 0; t < SPAN; ++t)
 #pragma unroll
           for (int e = 0; e < NV; ++e) xr[t][e] = 0.f;
+        #pragma unroll 1
         for (int s = 0; s < nin; ++s) {
           const View& vs = vin[s];
           const float w = awv[s];
@@ -487,6 +488,245 @@ __device__ __forceinline__ bool win_dispatch(const Problem& P, const View* views
     return false;
   }
   return true;
+}
+
+// Fused Relu-SepConv A operand. One 128 B channel chunk of a patch M tile (tN
+// images x tR rows x tWt columns, tile row r = (nn*tR + i)*tWt + j, as the epilogue maps it): the
+// producer warps compute ReLU(sum_i w_i x_i) -> k x k depthwise with the quad window walk of
+// win_tile and store the values, rounded to the storage precision (Z14), straight into the UMMA
+// SWIZZLE_NONE K-major layout [r/8][piece][r%8][16 B] the pointwise GEMM's MMAs read. The
+// depthwise output never goes to HBM and the pointwise half needs no dependency round.
+// Items = (quad of QW adjacent patch columns) x (16 B piece); 8 consecutive threads take the 8
+// pieces of one quad (coalesced 128 B loads of one pixel's chunk).
+template <int DT, int K, int S>
+__device__ __noinline__ void fdw_chunk(const Problem& P, const View* views, uint32_t dst, int chunk, int tn0,
+                                       int toh0, int tow0, int ptid) {
+  constexpr int NV = DT == ET_BF16 ? 8 : 4;
+  constexpr int QW = win_qw<DT>();
+  constexpr int SPAN = (QW - 1) * S + K;
+  const int tR = P.tR, tWt = P.tWt, nb = P.batch, Ho = P.Ho;
+  const int qwn = (tWt + QW - 1) / QW;
+  const int items = P.tN * tR * qwn * 8;
+  const View in = views[P.in_begin];
+  const int cs = in.C, inH = in.H, inW = in.W, dp = P.dp;
+  const float* wd = reinterpret_cast<const float*>(P.dww);
+  const int nin = min(P.n_in, 8);
+  View vin[8];
+  float awv[8];
+  {
+    const float* aw = reinterpret_cast<const float*>(P.add_w);
+    for (int s = 0; s < nin; ++s) {
+      vin[s] = views[P.in_begin + s];
+      awv[s] = aw ? __ldg(aw + s) : 1.0f;
+    }
+  }
+  for (int idx = ptid; idx < items; idx += 128) {
+    const int piece = idx & 7;
+    const int q = idx >> 3;
+    const int rowi = q / qwn;                  // nn * tR + i
+    const int qj = q - rowi * qwn;
+    const int nn = rowi / tR, i0 = rowi - nn * tR;
+    const int n = tn0 + nn, oh = toh0 + i0, ow0 = tow0 + qj * QW;
+    const int c = chunk * (8 * NV) + piece * NV;
+    float acc[QW][NV];
+#pragma unroll
+    for (int u = 0; u < QW; ++u)
+#pragma unroll
+      for (int e = 0; e < NV; ++e) acc[u][e] = 0.f;
+    if (n < nb && oh < Ho && c < cs) {
+      const int hs = oh * S - dp, ws = ow0 * S - dp;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const int ih = hs + i;
+        const bool rok = (unsigned)ih < (unsigned)inH;
+        const int64_t rowpix = ((int64_t)n * inH + (rok ? ih : 0)) * inW + ws;
+        float xr[SPAN][NV];
+        if (nin > 1) {
+#pragma unroll
+          for (int t = 0; t < SPAN; ++t)
+#pragma unroll
+            for (int e = 0; e < NV; ++e) xr[t][e] = 0.f;
+          #pragma unroll 1
+          for (int s = 0; s < nin; ++s) {
+            const View& vs = vin[s];
+            const float w = awv[s];
+#pragma unroll
+            for (int t = 0; t < SPAN; ++t) {
+              if (rok && (unsigned)(ws + t) < (unsigned)inW) {
+                float x[NV];
+                ld16<DT>(vs, rowpix + t, c, x);
+#pragma unroll
+                for (int e = 0; e < NV; ++e) xr[t][e] = fmaf(w, x[e], xr[t][e]);
+              }
+            }
+          }
+        } else {
+          const float w = awv[0];
+#pragma unroll
+          for (int t = 0; t < SPAN; ++t) {
+            if (rok && (unsigned)(ws + t) < (unsigned)inW) {
+              ld16<DT>(in, rowpix + t, c, xr[t]);
+#pragma unroll
+              for (int e = 0; e < NV; ++e) xr[t][e] *= w;
+            } else {
+#pragma unroll
+              for (int e = 0; e < NV; ++e) xr[t][e] = 0.f;
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < SPAN; ++t)
+#pragma unroll
+          for (int e = 0; e < NV; ++e) xr[t][e] = fmaxf(xr[t][e], 0.f);   // padding stays 0
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          float w[NV];
+          const float4* wp = reinterpret_cast<const float4*>(wd + (int64_t)(i * K + j) * cs + c);
+#pragma unroll
+          for (int h = 0; h < NV / 4; ++h) {
+            const float4 v = __ldg(wp + h);
+            w[4 * h] = v.x; w[4 * h + 1] = v.y; w[4 * h + 2] = v.z; w[4 * h + 3] = v.w;
+          }
+#pragma unroll
+          for (int u = 0; u < QW; ++u)
+#pragma unroll
+            for (int e = 0; e < NV; ++e) acc[u][e] = fmaf(w[e], xr[u * S + j][e], acc[u][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < QW; ++u) {
+      const int j = qj * QW + u;
+      if (j >= tWt) break;
+      const int r = rowi * tWt + j;
+      const uint32_t a = dst + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 16u + (uint32_t)piece * 128u;
+      uint32_t w4[4];
+      if (DT == ET_BF16) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[u][2 * h], acc[u][2 * h + 1]);
+          w4[h] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) w4[h] = __float_as_uint(tf32_round(acc[u][h]));
+      }
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w4[0]), "r"(w4[1]), "r"(w4[2]), "r"(w4[3])
+                   : "memory");
+    }
+  }
+}
+
+// Halo path of the fused Relu-SepConv (single input): the chunk's input window (hhs x hws pixels x
+// 128 B, dense [row][col][128 B], padding already zeros) and depthwise weights ([k*k][elems] fp32) sit
+// in shared memory; items as in fdw_chunk, every operand an ld.shared.v4.
+template <int DT, int K, int S>
+__device__ __noinline__ void fdw_halo(const Problem& P, uint32_t hbuf, uint32_t wbuf, uint32_t dst, int toh0, int ptid) {
+  constexpr int NV = DT == ET_BF16 ? 8 : 4;
+  constexpr int QW = win_qw<DT>();
+  constexpr int SPAN = (QW - 1) * S + K;
+  constexpr int ELEMS = 8 * NV;
+  const int tR = P.tR, tWt = P.tWt, hws = P.hws, Ho = P.Ho;
+  const int qwn = (tWt + QW - 1) / QW;
+  const int items = tR * qwn * 8;
+  const float* aw = reinterpret_cast<const float*>(P.add_w);
+  const float w0 = aw ? __ldg(aw) : 1.0f;
+  for (int idx = ptid; idx < items; idx += 128) {
+    const int piece = idx & 7;
+    const int q = idx >> 3;
+    const int i0 = q / qwn;
+    const int qj = q - i0 * qwn;
+    float acc[QW][NV];
+#pragma unroll
+    for (int u = 0; u < QW; ++u)
+#pragma unroll
+      for (int e = 0; e < NV; ++e) acc[u][e] = 0.f;
+    if (toh0 + i0 < Ho) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const uint32_t hrow = hbuf + (uint32_t)(((i0 * S + i) * hws + qj * QW * S) * 128 + piece * 16);
+        float xr[SPAN][NV];
+#pragma unroll
+        for (int t = 0; t < SPAN; ++t) {
+          uint32_t w[4];
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                       : "r"(hrow + t * 128));
+          if (DT == ET_BF16) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              xr[t][2 * h] = __uint_as_float(w[h] << 16);
+              xr[t][2 * h + 1] = __uint_as_float(w[h] & 0xffff0000u);
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) xr[t][h] = __uint_as_float(w[h]);
+          }
+#pragma unroll
+          for (int e = 0; e < NV; ++e) xr[t][e] = fmaxf(xr[t][e] * w0, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          float wv[NV];
+#pragma unroll
+          for (int h = 0; h < NV / 4; ++h) {
+            uint32_t w[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                         : "r"(wbuf + (uint32_t)(((i * K + j) * ELEMS + piece * NV + 4 * h) * 4)));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) wv[4 * h + e] = __uint_as_float(w[e]);
+          }
+#pragma unroll
+          for (int u = 0; u < QW; ++u)
+#pragma unroll
+            for (int e = 0; e < NV; ++e) acc[u][e] = fmaf(wv[e], xr[u * S + j][e], acc[u][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < QW; ++u) {
+      const int j = qj * QW + u;
+      if (j >= tWt) break;
+      const int r = i0 * tWt + j;
+      const uint32_t a = dst + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 16u + (uint32_t)piece * 128u;
+      uint32_t w4[4];
+      if (DT == ET_BF16) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[u][2 * h], acc[u][2 * h + 1]);
+          w4[h] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) w4[h] = __float_as_uint(tf32_round(acc[u][h]));
+      }
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w4[0]), "r"(w4[1]), "r"(w4[2]), "r"(w4[3])
+                   : "memory");
+    }
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void fdw_halo_dispatch(const Problem& P, uint32_t hbuf, uint32_t wbuf, uint32_t dst, int toh0,
+                                                  int ptid) {
+  const int k = P.dk, s = P.ds;
+  if (k == 3 && s == 1) fdw_halo<DT, 3, 1>(P, hbuf, wbuf, dst, toh0, ptid);
+  else if (k == 3 && s == 2) fdw_halo<DT, 3, 2>(P, hbuf, wbuf, dst, toh0, ptid);
+  else if (k == 5 && s == 1) fdw_halo<DT, 5, 1>(P, hbuf, wbuf, dst, toh0, ptid);
+  else if (k == 5 && s == 2) fdw_halo<DT, 5, 2>(P, hbuf, wbuf, dst, toh0, ptid);
+  else if (k == 7 && s == 1) fdw_halo<DT, 7, 1>(P, hbuf, wbuf, dst, toh0, ptid);
+  else fdw_halo<DT, 7, 2>(P, hbuf, wbuf, dst, toh0, ptid);
+}
+
+template <int DT>
+__device__ __forceinline__ void fdw_dispatch(const Problem& P, const View* views, uint32_t dst, int chunk, int tn0,
+                                             int toh0, int tow0, int ptid) {
+  const int k = P.dk, s = P.ds;
+  if (k == 3 && s == 1) fdw_chunk<DT, 3, 1>(P, views, dst, chunk, tn0, toh0, tow0, ptid);
+  else if (k == 3 && s == 2) fdw_chunk<DT, 3, 2>(P, views, dst, chunk, tn0, toh0, tow0, ptid);
+  else if (k == 5 && s == 1) fdw_chunk<DT, 5, 1>(P, views, dst, chunk, tn0, toh0, tow0, ptid);
+  else if (k == 5 && s == 2) fdw_chunk<DT, 5, 2>(P, views, dst, chunk, tn0, toh0, tow0, ptid);
+  else if (k == 7 && s == 1) fdw_chunk<DT, 7, 1>(P, views, dst, chunk, tn0, toh0, tow0, ptid);
+  else fdw_chunk<DT, 7, 2>(P, views, dst, chunk, tn0, toh0, tow0, ptid);   // planner: k in {3,5,7}, s in {1,2}
 }
 
 template <int DT>
@@ -668,14 +908,15 @@ __device__ __noinline__ void simt_tile(const Problem& P, const View* views, int 
 }
 
 // --------------------------------------------------------------------------------- the kernel
-struct Ring {          // smem ring iterator (slot, phase)
+struct Ring {          // smem ring iterator (slot, phase); n = slots this launch (StageDesc.ring_slots)
   int slot = 0;
   uint32_t phase = 0;
+  int n = kStages;
   __device__ __forceinline__ void advance(int n) {
     for (int i = 0; i < n; ++i) next();
   }
   __device__ __forceinline__ void next() {
-    if (++slot == kStages) {
+    if (++slot == n) {
       slot = 0;
       phase ^= 1u;
     }
@@ -706,6 +947,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   uint64_t* tempty = bars + 2 * kStages + 2;                // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* hbar = bars + 16;                               // halo + depthwise weights landed (halo path)
   float* sbias_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // 2 x kMaxBN
   uint8_t* sdesc = reinterpret_cast<uint8_t*>(bars) + kBarBytes + kBiasBytes;           // kDescBytes
   uint8_t* sepi = sdesc + kDescBytes;                                                     // kEpiBytes: 4 x 4 KB
@@ -765,6 +1007,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       mbar_init(smem_u32(&tfull[s]), 1);
       mbar_init(smem_u32(&tempty[s]), 128);
     }
+    mbar_init(smem_u32(hbar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp && sd.has_gemm && DT != ET_F32X) {
@@ -831,6 +1074,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     constexpr int ESZ = DT == ET_BF16 ? 2 : 4;
     constexpr int VEC = 16 / ESZ, ELEMS = kChunkBytes / ESZ;
     Ring ring;
+    ring.n = sd.ring_slots;
+    uint32_t hphase = 0;                        // halo barrier phase (fused Relu-SepConv, halo path)
     int hint = 0;
     for (int t = blockIdx.x; t < sd.n_tiles; t += gridDim.x) {
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
@@ -847,6 +1092,64 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const int nt = rest - mt * P.n_tiles_n;
       const int c0 = s * P.chunks_per_split;
       const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
+      if (DT != ET_F32X && P.fdw) {
+        // fused Relu-SepConv: depthwise computed into the A slot, pointwise weights by bulk copy
+        const int rr = fdiv(P.fd_tilw, mt);
+        const int tw = mt - rr * P.tiles_w;
+        const int tnn = fdiv(P.fd_tilh, rr);
+        const int tn0 = tnn * P.tN, toh0 = (rr - tnn * P.tiles_h) * P.tR, tow0 = tw * P.tWt;
+        const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)(nt * P.BN >> 3) * 1024;
+        const int64_t wstep = (int64_t)(P.Npad8 >> 3) * 1024;
+        const uint32_t bbytes = (uint32_t)min(P.BN, P.Npad8 - nt * P.BN) * kChunkBytes;
+        if (P.hws) {
+          // halo path: per chunk ONE 4D tensor TMA stages the tile's input window (padding = OOB
+          // zeros) and one bulk copy the chunk's depthwise weights; the items are then computed
+          // from shared memory (one load round per chunk instead of one per window row)
+          const uint32_t hbuf = smem_u32(sB + (kStages - 1) * kBStageBytes);
+          const uint32_t wbuf = smem_u32(sA + (kStages - 1) * kAStageBytes);
+          const uint32_t hbytes = (uint32_t)(P.hws * P.hhs) * kChunkBytes;
+          const uint32_t wbytes = (uint32_t)(P.dk * P.dk * kChunkBytes / ESZ) * 4u;
+          const int ih0 = toh0 * P.ds - P.dp, iw0 = tow0 * P.ds - P.dp;
+          for (int c = c0; c < c1; ++c) {
+            mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
+            named_bar(1, 128);   // every producer thread is done with the previous window
+            if (ptid == 0) {
+              const uint32_t fb = smem_u32(&full[ring.slot]);
+              mbar_arrive_expect_tx(fb, bbytes);
+              bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
+              mbar_arrive_expect_tx(smem_u32(hbar), hbytes + wbytes);
+              tma_load_4d(hbuf, P.tmap_a, c * ELEMS, iw0, ih0, tn0, smem_u32(hbar));
+              bulk_g2s(wbuf, reinterpret_cast<const uint8_t*>(P.dwc) + (int64_t)c * wbytes, wbytes, smem_u32(hbar));
+            }
+            mbar_wait(smem_u32(hbar), hphase);
+            hphase ^= 1u;
+            fdw_halo_dispatch<DT>(P, hbuf, wbuf, smem_u32(sA + ring.slot * kAStageBytes), toh0, ptid);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&full[ring.slot]));
+            ring.next();
+          }
+          if (ptid == 0 && tfirst) IOS_TRACE(12);
+          tfirst = false;
+          continue;
+        }
+        for (int c = c0; c < c1; ++c) {
+          mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
+          if (ptid == 0) {
+            const uint32_t fb = smem_u32(&full[ring.slot]);
+            mbar_arrive_expect_tx(fb, bbytes);
+            bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
+          }
+          fdw_dispatch<DT>(P, views, smem_u32(sA + ring.slot * kAStageBytes), c, tn0, toh0, tow0, ptid);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&full[ring.slot]));   // one arrival per producer warp
+          ring.next();
+        }
+        if (ptid == 0 && tfirst) IOS_TRACE(12);
+        tfirst = false;
+        continue;
+      }
       if (P.a_tma || P.tt) {
         // A is a plain [M, C] matrix (1x1, stride 1): ONE tensor TMA per chunk (128 rows x 128 B,
         // 128 B swizzle, rows past M / channels past C zero-filled) + one bulk copy for B, both
@@ -1046,6 +1349,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     // elected lane issues tcgen05.mma / tcgen05.commit.
     if (sd.has_gemm && DT != ET_F32X) {
       Ring ring;
+      ring.n = sd.ring_slots;
       int acc = 0;
       uint32_t acc_phase = 0;
       int hint = 0;
@@ -1059,7 +1363,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
         const uint32_t idesc = umma_idesc(DT == ET_BF16, P.BN);
         // the activation operand is 128 B-swizzled when TMA loads it; swap-AB puts it in the B slot
-        const bool act_tma = P.a_tma != 0 || P.tt != 0;
+        const bool act_tma = (P.a_tma != 0 || P.tt != 0) && !P.fdw;
         const bool a_sw128 = act_tma && !P.swap_ab;
         const bool b_sw128 = act_tma && P.swap_ab;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1u);
@@ -1092,6 +1396,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     // ============================================================== EPILOGUE + SIMT (warps 4-7)
     const int etid = tid - kEpilogueWarp0 * 32;   // 0..127 == TMEM lane == tile row
     Ring ering;                                   // FP32-SIMT mode: the epilogue consumes the smem ring
+    ering.n = sd.ring_slots;
     const int lane_base = (warp & 3) * 32;        // TMEM lanes this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -1221,8 +1526,13 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         } else {
           // split-K: fp32 accumulator channel-major [128 channels][BN pixels]; each thread adds its
           // channel's 16 pixels per TMEM load with four 16 B vector reductions (pixels past M add 0)
-          float* tacc = reinterpret_cast<float*>(P.workspace) + (int64_t)out_tile * kBM * BNx;
+          // split s writes its partial into its own slab [S][128][BN] of the tile (plain stores:
+          // L2 write bandwidth, no atomics); the finalize sums the S slabs in a fixed order
+          // (deterministic)
+          const int64_t slab = (int64_t)kBM * BNx;
+          float* tacc = reinterpret_cast<float*>(P.workspace) + (int64_t)out_tile * slab * P.split;
           float* trow = tacc + (int64_t)etid * BNx;
+          float* mrow = trow + s * slab;
           for (int c0 = 0; c0 < BNx; c0 += 16) {
             uint32_t v[16];
             tmem_ld16(tbase + c0, v);
@@ -1232,9 +1542,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               if (c0 + j >= Mx) v[j] = 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              if (c0 + 4 * q < Mx)
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(trow + c0 + 4 * q), "r"(v[4 * q]),
-                             "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3]));
+              if (c0 + 4 * q < Mx) stg_v4(mrow + c0 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           }
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty[acc]));
@@ -1242,22 +1550,36 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep);
           named_bar(2, 128);
           // distributed finalize: split s owns pixel quads [s*np4/S, (s+1)*np4/S) of the tile; each
-          // thread reads its channel's quads (float4, 8 in flight), re-zeroes them, and emits them
+          // thread sums its channel's quads over the S slabs (16 float4 in flight) and emits them
           // through the staged vector stores. Reading lines other SMs just reduced into is slow,
           // so the S splits share the read-back instead of one last-arriving CTA doing it all.
           const int np4 = (Mx + 3) >> 2;
           const int kq0 = s * np4 / P.split, kq1 = (s + 1) * np4 / P.split;
           if (etid == 0) IOS_TRACE(13);
-          for (int k0 = kq0; k0 < kq1; k0 += 8) {
-            float4 x[8];
+          for (int k0 = kq0; k0 < kq1; k0 += 4) {
+            float4 x[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (k0 + u < kq1) x[u] = __ldcg(reinterpret_cast<const float4*>(trow) + k0 + u);
+            for (int u = 0; u < 4; ++u) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j0 = 0; j0 < P.split; j0 += 4) {   // 4 quads x 4 slabs in flight
+              float4 t[4][4];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  t[jj][u] = (j0 + jj < P.split && k0 + u < kq1)
+                                 ? __ldcg(reinterpret_cast<const float4*>(trow + (j0 + jj) * slab) + k0 + u)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  x[u].x += t[jj][u].x; x[u].y += t[jj][u].y; x[u].z += t[jj][u].z; x[u].w += t[jj][u].w;
+                }
+            }
             if (etid == 0 && k0 == kq0) IOS_TRACE(14);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 4; ++u) {
               if (k0 + u >= kq1) break;
-              stg_zero4_cg(reinterpret_cast<float4*>(trow) + k0 + u);
               float o[4] = {x[u].x + bv, x[u].y + bv, x[u].z + bv, x[u].w + bv};
               if (relu) {
 #pragma unroll
@@ -1421,11 +1743,13 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         tc_fence_before();
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
       } else {
-        // split-K: every split adds its fp32 partial into the tile's zeroed accumulator with
-        // vector reductions (fire-and-forget at L2); the last arriving split reads the sum once,
-        // applies bias/ReLU, stores, and re-zeroes the accumulator for the next launch.
+        // split-K: every split stores its fp32 partial into its own slab of the tile (plain
+        // coalesced stores; L2 atomics were throughput-bound), all splits rendezvous, and each
+        // finalizes 1/S of the tile: sum of the S slabs in split order (deterministic), bias/ReLU.
         float* ws = reinterpret_cast<float*>(P.workspace);
-        float* tacc = ws + (int64_t)out_tile * kBM * BNx;     // [kBM][BN] fp32 accumulator
+        const int64_t slab = (int64_t)kBM * BNx;
+        float* tacc = ws + (int64_t)out_tile * slab * P.split;  // [S][kBM][BN] fp32 partials
+        float* macc = tacc + s * slab;                          // this split's slab
         const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
         const int wr0 = (warp & 3) * 32;
         for (int c0 = 0; c0 < BNx; c0 += 32) {
@@ -1448,41 +1772,55 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
                          : "r"(stg + r * 128 + ((p ^ (r & 7)) * 16)));
             const int col = c0 + p * 4;
-            if (wr0 + r < trows && col < BNx)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(tacc + (wr0 + r) * BNx + col),
-                           "r"(w0), "r"(w1), "r"(w2), "r"(w3) );
+            if (wr0 + r < trows && col < BNx) stg_v4(macc + (wr0 + r) * BNx + col, w0, w1, w2, w3);
           }
           __syncwarp();
         }
         tc_fence_before();
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
         named_bar(2, 128);
+        if (etid == 0 && tfirst) IOS_TRACE(13);
         if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep);
         named_bar(2, 128);
+        if (etid == 0 && tfirst) IOS_TRACE(14);
         {
           // distributed finalize (see the swap-AB path): split s owns tile rows
           // [s*trows/S, (s+1)*trows/S); all 128 threads, coalesced (consecutive threads sweep a
-          // row's contiguous columns), re-zeroing the accumulator for the next launch
+          // row's contiguous columns)
           const int bn = BNx, q4 = bn / 4;
           const int r0 = s * trows / P.split, r1 = (s + 1) * trows / P.split;
           const int total = (r1 - r0) * q4;
-          // 8 independent float4 loads in flight per thread per round (the accumulator sits in L2)
-          for (int base = etid; base < total; base += 128 * 8) {
-            float4 x[8];
+          // 4 elements x 4 slabs = 16 independent float4 loads in flight per thread (L2-resident)
+          for (int base = etid; base < total; base += 128 * 4) {
+            float4 x[4];
+            int off[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 4; ++u) {
               const int idx = base + u * 128;
-              if (idx < total) {
-                const int r = r0 + idx / q4, col = (idx % q4) * 4;
-                x[u] = __ldcg(reinterpret_cast<const float4*>(tacc + r * bn + col));
-              }
+              off[u] = idx < total ? (r0 + idx / q4) * bn + (idx % q4) * 4 : -1;
+              x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (int j0 = 0; j0 < P.split; j0 += 4) {
+              float4 t[4][4];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  t[jj][u] = (j0 + jj < P.split && off[u] >= 0)
+                                 ? __ldcg(reinterpret_cast<const float4*>(tacc + (j0 + jj) * slab + off[u]))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  x[u].x += t[jj][u].x; x[u].y += t[jj][u].y; x[u].z += t[jj][u].z; x[u].w += t[jj][u].w;
+                }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 4; ++u) {
               const int idx = base + u * 128;
               if (idx >= total) break;
               const int r = r0 + idx / q4, col = (idx % q4) * 4;
-              stg_zero4_cg(tacc + r * bn + col);
               const int ncol = nt * bn + col;
               const Segment* sgp = &segs[P.seg_begin];
               if (P.n_seg > 1) {

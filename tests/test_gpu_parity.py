@@ -136,3 +136,24 @@ def test_conv_zoo_im2col_paths(torch_cuda, batch, hw, math):
     torch_cuda.cuda.synchronize()
     errs = per_op_errors(net, g, math, ops=[12, 13, 14])
     assert max(errs.values()) < TOL[math], errs
+
+
+@pytest.mark.parametrize("batch,hw,math", [(1, 37, "tf32"), (1, 37, "bf16"), (2, 7, "tf32"), (3, 9, "bf16"),
+                                           (1, 150, "bf16"), (1, 83, "tf32")])
+def test_sepconv_zoo_fused_depthwise(torch_cuda, batch, hw, math):
+    """Fused Relu-SepConv (the depthwise half computed by the producer warps into the
+    pointwise GEMM's A operand): every window / stride / aggregation / patch-geometry class, per op
+    under the sequential schedule, then the whole block as ONE concurrent stage (the chain waits on
+    an in-kernel counter)."""
+    net = W.build("sepconv_zoo", batch=batch, hw=hw, math=math)
+    ref = OracleGraph(net).run_sequential(net.make_input())[net.n_ops]
+    g, q, y = _run(net, math, "sequential", torch_cuda)
+    errs = per_op_errors(net, g, math)
+    worst = max(errs, key=errs.get)
+    assert errs[worst] < TOL[math], (worst, net.op(worst).name, errs[worst])
+    assert rel_err(y, ref) < TOL[math]
+    g2, _, y2 = _run(net, math, [(list(range(1, net.n_ops + 1)), 0)], torch_cuda)
+    errs = per_op_errors(net, g2, math)
+    worst = max(errs, key=errs.get)
+    assert errs[worst] < TOL[math], (worst, net.op(worst).name, errs[worst])
+    assert rel_err(y2, ref) < TOL[math]

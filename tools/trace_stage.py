@@ -18,7 +18,7 @@ for ops, t in stages:
     t0 = a[:, 0][a[:, 0] > 0].min()
     rel = np.where(a > 0, (a - t0) / 1000.0, np.nan)
     print(f"stage {ops} T={t} profiled {ms*1e3:.1f} us, grid {grid.value}; us since first entry (min/median/max over CTAs):")
-    names = ["entry", "prologue", "A1 issued", "prod done", "mma done", "acc1 ready", "epi done", "teardown", "exit", "A2 issued", "A3 issued", "own prologue", "A landed", "e:tmem1", "e:staged1", "e:stored1"]
+    names = ["entry", "prologue", "A1 issued", "prod done", "mma done", "acc1 ready", "epi done", "teardown", "exit", "A2 issued", "A3 issued", "own prologue", "A landed", "e:reds issued", "e:rendezvous", "e:stored1"]
     for k, nm in enumerate(names):
         col = rel[:, k]
         col = col[~np.isnan(col)]

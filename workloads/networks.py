@@ -95,6 +95,27 @@ def conv_zoo_net(seed: int = 11, batch: int = 1, math: str = "tf32", hw: int = 3
     return nb.net
 
 
+def sepconv_zoo_net(seed: int = 13, batch: int = 1, math: str = "tf32", hw: int = 37, cin: int = 40) -> NetSpec:
+    """Relu-SepConv shape zoo (parity tests of the fused depthwise->pointwise GEMM; not
+    a paper workload): k in {3, 5, 7} x stride {1, 2}, a channel count that leaves a partial K chunk,
+    weighted multi-input aggregation (negative weights: the ReLU follows the sum), Cout > 256 (two
+    N tiles), a sepconv chain and a post-ReLU unit."""
+    nb = NetBuilder("sepconv_zoo", (batch, cin, hw, hw), seed, math)
+    nb.new_block()
+    x1 = nb.conv(0, cin, 1, relu=False, name="pre")
+    nb.sepconv(0, 48, 3, 1, name="k3s1")
+    nb.sepconv(0, 40, 3, 2, name="k3s2")
+    s5 = nb.sepconv(0, 56, 5, 1, name="k5s1")
+    nb.sepconv(0, 24, 5, 2, name="k5s2")
+    nb.sepconv(0, 32, 7, 1, name="k7s1")
+    nb.sepconv(0, 40, 7, 2, name="k7s2")
+    nb.sepconv([0, x1], 40, 3, 1, add_weights=[0.5, -0.8], name="agg2")
+    nb.sepconv([x1, 0, x1], 32, 5, 2, add_weights=[1.3, 0.4, -0.2], name="agg3s2")
+    nb.sepconv(s5, 48, 3, 1, relu_post=True, name="chain")
+    nb.sepconv(0, 300, 3, 1, name="wide")
+    return nb.net
+
+
 # --------------------------------------------------------------------------------------------
 # Inception V3 (torchvision topology; Conv-Relu units, BN folded into bias)
 # --------------------------------------------------------------------------------------------
@@ -398,6 +419,7 @@ NETWORKS: Dict[str, Callable[..., NetSpec]] = {
     "fig5": fig5_graph,
     "tiny_mixed": tiny_mixed_net,
     "conv_zoo": conv_zoo_net,
+    "sepconv_zoo": sepconv_zoo_net,
     "inception_v3": inception_v3,
     "squeezenet": squeezenet,
     "nasnet_a_large": nasnet_a_large,
