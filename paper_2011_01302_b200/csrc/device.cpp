@@ -343,13 +343,15 @@ struct GemmSpec {
   int swap;   // swap-AB: weights are the 128-row MMA operand, the (<= 128) pixels are N
   int max_bn = kMaxBN;
   int tt_tiles = 0;   // tap-TMA: number of patch M tiles (0 = dense 128-pixel tiles)
-  int fdw = 0;        // fused Relu-SepConv: split K down to one chunk, never narrow N (each N tile
+  int fdw = 0;        // fused Relu-SepConv (1 register form: split K down to one chunk; 2 halo form:
+                      // never split K, the CTA pipelines its chunks); never narrow N (each N tile
                       // would recompute the depthwise half)
   double chunk_cost = 1.0;   // relative cost of one K chunk (fused depthwise chunks are compute)
 };
 
 // Fused Relu-SepConv eligibility: square window k in {3, 5, 7}, stride 1-2, at most
 // 8 aggregated inputs, tcgen05 math modes (FP32-SIMT keeps the two-problem form)
+TTGeom halo_geometry(int batch, int Ho, int Wo, int k, int s, int qw);
 bool fuse_dw_ok(const Graph& g, const Op& o) {
   static const bool on = [] {
     const char* v = getenv("IOS_FUSE_DW");
@@ -364,6 +366,17 @@ bool fuse_dw_ok(const Graph& g, const Op& o) {
   // multi-input units (RandWire aggregation) have no halo path: their register-window form is
   // slower than the two-problem form, so they stay unfused unless IOS_FUSE_DW=2
   if (o.inputs.size() > 1 && !(getenv("IOS_FUSE_DW") && atoi(getenv("IOS_FUSE_DW")) >= 2)) return false;
+  // halo path: one chunk's depthwise weights (k*k x 128 B of channels, held as fp32) in 8 KB
+  if (o.inputs.size() == 1 && o.kh * o.kw * (kChunkBytes / g.esize()) * 4 > kHaloWBytes / 2) return false;
+  if (o.inputs.size() == 1) {
+    // measured (tools/op_report.py, NASNet-A / RandWire, 1 B200): fusion pays for 5x5/7x7 windows
+    // and strided 3x3; a 3x3 stride-1 depthwise is cheap enough that the separate SIMT tile spread
+    // over all SMs wins; windows whose 16 KB halo leaves patch tiles under 32 pixels (7x7 stride
+    // 2) would launch hundreds of tiny tiles
+    if (o.kh == 3 && o.sh == 1 && !(getenv("IOS_FUSE_DW") && atoi(getenv("IOS_FUSE_DW")) >= 3)) return false;
+    const TTGeom tg = halo_geometry(g.batch, o.H, o.W, o.kh, o.sh, g.math == IOS_MATH_BF16 ? 2 : 4);
+    if (tg.tR * tg.tWt < 32) return false;
+  }
   return true;
 }
 
@@ -379,7 +392,7 @@ TTGeom halo_geometry(int batch, int Ho, int Wo, int k, int s, int qw) {
     const int qpr = (wt + qw - 1) / qw;
     for (int r = std::min(Ho, kBM / wt); r >= 1; --r) {
       const int hs = (r - 1) * s + k;
-      if (hs > 256 || ws * hs * kChunkBytes > kHaloBytes || qpr * r > 32) continue;
+      if (hs > 256 || ws * hs * kChunkBytes > kHaloBytes / 2 || qpr * r > 32) continue;
       const int th = (Ho + r - 1) / r, tw = (Wo + wt - 1) / wt;
       const int tiles = batch * th * tw;
       const int px = r * wt;
@@ -418,6 +431,7 @@ struct TileKnobs {
   int min_bn;         // narrowest N tile otherwise
   int one_wave;       // never refine past the target unit count (one wave of CTAs)
   int simt_in_target; // count SIMT tiles toward the target
+  int max_split;      // most K splits per GEMM
 };
 static TileKnobs tile_knobs() {
   static TileKnobs k = [] {
@@ -426,7 +440,8 @@ static TileKnobs tile_knobs() {
       return v ? atoi(v) : d;
     };
     return TileKnobs{env("IOS_TARGET_UNITS", 0), env("IOS_MIN_CPS", 4), env("IOS_MIN_BN_SMALL", 16),
-                     env("IOS_MIN_BN", 32), env("IOS_ONE_WAVE", 1), env("IOS_SIMT_IN_TARGET", 0)};
+                     env("IOS_MIN_BN", 32), env("IOS_ONE_WAVE", 1), env("IOS_SIMT_IN_TARGET", 0),
+                     env("IOS_MAX_SPLIT", 32)};
   }();
   return k;
 }
@@ -470,7 +485,8 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       const int min_bn = p->mt <= 2 ? kn.min_bn_small : kn.min_bn;
       const int min_cps = p->fdw ? 1 : kn.min_cps;
       const bool can_n = !p->swap && !p->fdw && p->BN >= 2 * min_bn;
-      const bool can_k = p->cps >= 2 * min_cps && p->split < 32;
+      // halo-path fused units pipeline their chunks in one CTA (no split-K finalize round)
+      const bool can_k = p->cps >= 2 * min_cps && p->split < kn.max_split && p->fdw != 2;
       if (!can_n && !can_k) continue;
       const double c = p->cps * p->chunk_cost * (1.0 + p->BN / 256.0);
       if (c > best_cost) {
@@ -489,7 +505,7 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
       best->BN = round_up(best->BN / 2, 16);
       best->ntn = (best->N16 + best->BN - 1) / best->BN;
     } else {
-      int want = best->split * 2;
+      int want = std::min(best->split * 2, kn.max_split);
       const int room = (target - others) / (best->mt * best->ntn);
       if (kn.one_wave && want > room) want = room;
       if (want <= best->split || (best->kch + want - 1) / want < best_min_cps) break;
@@ -714,7 +730,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
               p.dww = (uint64_t)e.dw;
               p.add_w = (uint64_t)e.add_w;
               const int qw = g.math == IOS_MATH_BF16 ? 2 : 4;
-              const bool halo = o.inputs.size() == 1;
+              const bool halo = o.inputs.size() == 1;   // fuse_dw_ok admits multi-input units only with IOS_FUSE_DW=2
               const TTGeom tg = halo ? halo_geometry(g.batch, o.H, o.W, o.kh, o.sh, qw) : fdw_geometry(g.batch, o.H, o.W, qw);
               if (halo) {
                 p.hws = (tg.tWt - 1) * o.sw + o.kw;
@@ -727,7 +743,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
               GemmSpec& sp = b.specs[pi];
               sp.tt_tiles = tg.tiles;
               sp.swap = 0;
-              sp.fdw = 1;
+              sp.fdw = halo ? 2 : 1;
               sp.chunk_cost = 1.0 + o.kh * o.kw / 4.0;
               b.seg(pi, 0, o.Cp, e.out, (o.flags & IOS_F_RELU_POST) ? 1 : 0);
               b.add_deps(pi, deps);
@@ -837,7 +853,10 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
       p.n_tiles = s.mt * s.ntn * s.split;
       if (p.split > 1) {
         p.workspace = ws_bytes;   // offset for now
-        ws_bytes += (size_t)s.mt * s.ntn * s.split * kBM * s.BN * sizeof(float);   // one fp32 partial slab per split
+        // one fp32 partial slab per split (<= kSlabSplits), else one zeroed reduction slab
+        static const int slab_splits = getenv("IOS_SLAB_SPLITS") ? atoi(getenv("IOS_SLAB_SPLITS")) : kSlabSplits;
+        p.slabs = s.split <= slab_splits ? 1 : 0;
+        ws_bytes += (size_t)s.mt * s.ntn * (p.slabs ? s.split : 1) * kBM * s.BN * sizeof(float);
         p.tilectr_idx = n_tilectr;
         n_tilectr += s.mt * s.ntn;
       }

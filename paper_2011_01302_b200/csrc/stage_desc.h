@@ -25,6 +25,11 @@ constexpr int kMmaWarp = 8;               // warp 8: tcgen05.mma issuer + TMEM a
 constexpr int kThreads = 9 * 32;
 constexpr int kTmemCols = 512;            // 2 accumulator buffers x 256 columns
 constexpr int kMaxProblems = 96;
+constexpr int kSlabSplits = 1;            // split-K: problems with <= this many splits store per-split
+                                          // slabs summed in split order (deterministic); the others reduce
+                                          // into one zeroed slab (red.add: measured faster at every split
+                                          // count, so the default is 1 = always reduce; IOS_SLAB_SPLITS=32
+                                          // is the deterministic mode)
 constexpr int kMaxSegs = 8;               // merged conv: one output segment per branch
 
 enum ProblemKind : int32_t {
@@ -86,8 +91,11 @@ struct Problem {
   int32_t Npad8;                    // packed weight rows (multiple of 8)
   int32_t seg_begin, n_seg;
   uint64_t workspace;               // split-K fp32 partials, per output tile [split][kBM][BN] (swap-AB:
-                                    // channel-major [split][128][BN]); summed in split order
+                                    // channel-major [split][128][BN]), summed in split order; with more
+                                    // than kSlabSplits splits one zeroed [kBM][BN] slab that the splits
+                                    // reduce into (red.add) and the finalize re-zeroes
   int32_t tilectr_idx;              // split-K arrival counters base
+  int32_t slabs;                    // split-K: 1 per-split slabs, 0 one reduction slab (see workspace)
   int32_t signal;                   // 1: a later member of the stage waits on done_idx
   FastDiv fd_howo, fd_wo, fd_split, fd_ntn, fd_cin, fd_kw;   // divisors of the tile / im2col decode
   // SIMT geometry

@@ -222,6 +222,9 @@ __device__ __forceinline__ void stg_v2(void* p, uint32_t a, uint32_t b) {
 __device__ __forceinline__ void stg_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d));
 }
+__device__ __forceinline__ void red_add_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 __device__ __forceinline__ void stg_zero4_cg(void* p) {
   asm volatile("st.global.cg.v4.b32 [%0], {%1, %1, %1, %1};" ::"l"(p), "r"(0));
 }
@@ -947,7 +950,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   uint64_t* tempty = bars + 2 * kStages + 2;                // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
-  uint64_t* hbar = bars + 16;                               // halo + depthwise weights landed (halo path)
+  uint64_t* hbar = bars + 16;                               // [2] halo + depthwise weights landed (halo path)
   float* sbias_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // 2 x kMaxBN
   uint8_t* sdesc = reinterpret_cast<uint8_t*>(bars) + kBarBytes + kBiasBytes;           // kDescBytes
   uint8_t* sepi = sdesc + kDescBytes;                                                     // kEpiBytes: 4 x 4 KB
@@ -1007,7 +1010,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       mbar_init(smem_u32(&tfull[s]), 1);
       mbar_init(smem_u32(&tempty[s]), 128);
     }
-    mbar_init(smem_u32(hbar), 1);
+    mbar_init(smem_u32(&hbar[0]), 1);
+    mbar_init(smem_u32(&hbar[1]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp && sd.has_gemm && DT != ET_F32X) {
@@ -1104,26 +1108,36 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         if (P.hws) {
           // halo path: per chunk ONE 4D tensor TMA stages the tile's input window (padding = OOB
           // zeros) and one bulk copy the chunk's depthwise weights; the items are then computed
-          // from shared memory (one load round per chunk instead of one per window row)
-          const uint32_t hbuf = smem_u32(sB + (kStages - 1) * kBStageBytes);
-          const uint32_t wbuf = smem_u32(sA + (kStages - 1) * kAStageBytes);
+          // from shared memory. Double-buffered: chunk c+1's window is in flight while chunk c is
+          // computed (slot 3's B region = 2 windows of 16 KB, its A region = 2 x 8 KB of weights).
+          const uint32_t hbuf0 = smem_u32(sB + (kStages - 1) * kBStageBytes);
+          const uint32_t wbuf0 = smem_u32(sA + (kStages - 1) * kAStageBytes);
           const uint32_t hbytes = (uint32_t)(P.hws * P.hhs) * kChunkBytes;
           const uint32_t wbytes = (uint32_t)(P.dk * P.dk * kChunkBytes / ESZ) * 4u;
           const int ih0 = toh0 * P.ds - P.dp, iw0 = tow0 * P.ds - P.dp;
+          auto issue = [&](int c, int b) {
+            const uint32_t hb = smem_u32(&hbar[b]);
+            mbar_arrive_expect_tx(hb, hbytes + wbytes);
+            tma_load_4d(hbuf0 + b * (kHaloBytes / 2), P.tmap_a, c * ELEMS, iw0, ih0, tn0, hb);
+            bulk_g2s(wbuf0 + b * (kHaloWBytes / 2), reinterpret_cast<const uint8_t*>(P.dwc) + (int64_t)c * wbytes, wbytes,
+                     hb);
+          };
+          named_bar(1, 128);   // every producer thread is done with the previous tile's windows
+          if (ptid == 0) issue(c0, 0);
           for (int c = c0; c < c1; ++c) {
+            const int b = (c - c0) & 1;
             mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
-            named_bar(1, 128);   // every producer thread is done with the previous window
+            if (c > c0) named_bar(1, 128);   // chunk c-1 (buffer b^1) fully consumed
             if (ptid == 0) {
               const uint32_t fb = smem_u32(&full[ring.slot]);
               mbar_arrive_expect_tx(fb, bbytes);
               bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
-              mbar_arrive_expect_tx(smem_u32(hbar), hbytes + wbytes);
-              tma_load_4d(hbuf, P.tmap_a, c * ELEMS, iw0, ih0, tn0, smem_u32(hbar));
-              bulk_g2s(wbuf, reinterpret_cast<const uint8_t*>(P.dwc) + (int64_t)c * wbytes, wbytes, smem_u32(hbar));
+              if (c + 1 < c1) issue(c + 1, b ^ 1);
             }
-            mbar_wait(smem_u32(hbar), hphase);
-            hphase ^= 1u;
-            fdw_halo_dispatch<DT>(P, hbuf, wbuf, smem_u32(sA + ring.slot * kAStageBytes), toh0, ptid);
+            mbar_wait(smem_u32(&hbar[b]), (hphase >> b) & 1u);
+            hphase ^= 1u << b;
+            fdw_halo_dispatch<DT>(P, hbuf0 + b * (kHaloBytes / 2), wbuf0 + b * (kHaloWBytes / 2),
+                                  smem_u32(sA + ring.slot * kAStageBytes), toh0, ptid);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&full[ring.slot]));
@@ -1530,9 +1544,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           // L2 write bandwidth, no atomics); the finalize sums the S slabs in a fixed order
           // (deterministic)
           const int64_t slab = (int64_t)kBM * BNx;
-          float* tacc = reinterpret_cast<float*>(P.workspace) + (int64_t)out_tile * slab * P.split;
+          const bool slabs = P.slabs != 0;   // else: vector reductions into one zeroed slab
+          float* tacc = reinterpret_cast<float*>(P.workspace) + (int64_t)out_tile * slab * (slabs ? P.split : 1);
           float* trow = tacc + (int64_t)etid * BNx;
-          float* mrow = trow + s * slab;
+          float* mrow = trow + (slabs ? s * slab : 0);
           for (int c0 = 0; c0 < BNx; c0 += 16) {
             uint32_t v[16];
             tmem_ld16(tbase + c0, v);
@@ -1542,7 +1557,12 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               if (c0 + j >= Mx) v[j] = 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              if (c0 + 4 * q < Mx) stg_v4(mrow + c0 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              if (c0 + 4 * q < Mx) {
+                if (slabs)
+                  stg_v4(mrow + c0 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                else
+                  red_add_v4(mrow + c0 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              }
           }
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty[acc]));
@@ -1560,13 +1580,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             float4 x[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int j0 = 0; j0 < P.split; j0 += 4) {   // 4 quads x 4 slabs in flight
+            const int nsl = slabs ? P.split : 1;
+            for (int j0 = 0; j0 < nsl; j0 += 4) {   // 4 quads x 4 slabs in flight
               float4 t[4][4];
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                  t[jj][u] = (j0 + jj < P.split && k0 + u < kq1)
+                  t[jj][u] = (j0 + jj < nsl && k0 + u < kq1)
                                  ? __ldcg(reinterpret_cast<const float4*>(trow + (j0 + jj) * slab) + k0 + u)
                                  : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -1580,6 +1601,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               if (k0 + u >= kq1) break;
+              if (!slabs) stg_zero4_cg(reinterpret_cast<float4*>(trow) + k0 + u);   // re-zero for the next launch
               float o[4] = {x[u].x + bv, x[u].y + bv, x[u].z + bv, x[u].w + bv};
               if (relu) {
 #pragma unroll
@@ -1748,8 +1770,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // finalizes 1/S of the tile: sum of the S slabs in split order (deterministic), bias/ReLU.
         float* ws = reinterpret_cast<float*>(P.workspace);
         const int64_t slab = (int64_t)kBM * BNx;
-        float* tacc = ws + (int64_t)out_tile * slab * P.split;  // [S][kBM][BN] fp32 partials
-        float* macc = tacc + s * slab;                          // this split's slab
+        const bool slabs = P.slabs != 0;                         // else: reductions into one zeroed slab
+        float* tacc = ws + (int64_t)out_tile * slab * (slabs ? P.split : 1);  // [S][kBM][BN] fp32 partials
+        float* macc = tacc + (slabs ? s * slab : 0);            // this split's slab
         const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
         const int wr0 = (warp & 3) * 32;
         for (int c0 = 0; c0 < BNx; c0 += 32) {
@@ -1772,7 +1795,12 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
                          : "r"(stg + r * 128 + ((p ^ (r & 7)) * 16)));
             const int col = c0 + p * 4;
-            if (wr0 + r < trows && col < BNx) stg_v4(macc + (wr0 + r) * BNx + col, w0, w1, w2, w3);
+            if (wr0 + r < trows && col < BNx) {
+              if (slabs)
+                stg_v4(macc + (wr0 + r) * BNx + col, w0, w1, w2, w3);
+              else
+                red_add_v4(macc + (wr0 + r) * BNx + col, w0, w1, w2, w3);
+            }
           }
           __syncwarp();
         }
@@ -1790,7 +1818,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           const int bn = BNx, q4 = bn / 4;
           const int r0 = s * trows / P.split, r1 = (s + 1) * trows / P.split;
           const int total = (r1 - r0) * q4;
-          // 4 elements x 4 slabs = 16 independent float4 loads in flight per thread (L2-resident)
+          // 4 elements x 4 slabs = 16 independent float4 loads in flight per thread
           for (int base = etid; base < total; base += 128 * 4) {
             float4 x[4];
             int off[4];
@@ -1800,13 +1828,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               off[u] = idx < total ? (r0 + idx / q4) * bn + (idx % q4) * 4 : -1;
               x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            for (int j0 = 0; j0 < P.split; j0 += 4) {
+            const int nsl = slabs ? P.split : 1;
+            for (int j0 = 0; j0 < nsl; j0 += 4) {
               float4 t[4][4];
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                  t[jj][u] = (j0 + jj < P.split && off[u] >= 0)
+                  t[jj][u] = (j0 + jj < nsl && off[u] >= 0)
                                  ? __ldcg(reinterpret_cast<const float4*>(tacc + (j0 + jj) * slab + off[u]))
                                  : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -1821,6 +1850,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               const int idx = base + u * 128;
               if (idx >= total) break;
               const int r = r0 + idx / q4, col = (idx % q4) * 4;
+              if (!slabs) stg_zero4_cg(tacc + off[u]);   // re-zero for the next launch
               const int ncol = nt * bn + col;
               const Segment* sgp = &segs[P.seg_begin];
               if (P.n_seg > 1) {

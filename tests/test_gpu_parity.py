@@ -157,3 +157,30 @@ def test_sepconv_zoo_fused_depthwise(torch_cuda, batch, hw, math):
     worst = max(errs, key=errs.get)
     assert errs[worst] < TOL[math], (worst, net.op(worst).name, errs[worst])
     assert rel_err(y2, ref) < TOL[math]
+
+
+def test_deterministic_split_k_slabs(torch_cuda):
+    """IOS_SLAB_SPLITS=32: every split-K problem stores per-split slabs that the finalize sums in
+    split order, so repeated runs are bitwise identical (SURVEY §5 determinism mode); parity holds.
+    Runs in a subprocess because the library reads the knob once per process."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import hashlib, numpy as np, torch, workloads as W
+from paper_2011_01302_b200 import Graph
+net = W.build("conv_zoo", batch=1, hw=37, math="tf32")
+g = Graph.from_netspec(net, "tf32")
+q = g.schedule_sequential()
+x = torch.from_numpy(net.make_input()).cuda()
+hs = []
+for _ in range(3):
+    g.run(q, x); torch.cuda.synchronize()
+    hs.append(hashlib.sha1(b"".join(g.op_output(i).cpu().numpy().tobytes() for i in range(1, net.n_ops + 1))).hexdigest())
+print(len(set(hs)))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IOS_SLAB_SPLITS="32", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == "1", out.stdout
