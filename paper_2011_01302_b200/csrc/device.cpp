@@ -196,21 +196,13 @@ TTGeom fdw_geometry(int batch, int Ho, int Wo, int qw) {
 }
 
 // Tap-TMA im2col eligibility: returns the number of 128 B channel blocks per tap (0 = use the
-// cp.async gather or the 2D TMA path). Pre-ReLU convs take it too (the producers apply the ReLU
-// in smem once the box lands); 1x1/s1/unpadded convs take the plain 2D TMA; narrow inputs would pad K too much;
+// cp.async gather or the 2D TMA path). Pre-ReLU convs need the gather (the ReLU is applied on the
+// way to smem); 1x1/s1/unpadded convs take the plain 2D TMA; narrow inputs would pad K too much;
 // patch tiles must not waste much more M than the gather's dense 128-pixel tiles.
 bool tap_tma_enabled();
-// pre-ReLU convs on the TMA paths (ReLU applied in smem by the producer warps); IOS_RELU_TMA=0: gather
-bool relu_tma_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("IOS_RELU_TMA");
-    return v ? atoi(v) != 0 : true;
-  }();
-  return on;
-}
 int tap_tma_blocks(const Graph& g, int cin_p, int kh, int kw, int sh, int sw, int ph, int pw, int flags, int batch,
                    int Ho, int Wo) {
-  if (g.math == IOS_MATH_FP32_SIMT || ((flags & IOS_F_RELU_PRE) && !relu_tma_enabled())) return 0;
+  if (g.math == IOS_MATH_FP32_SIMT || (flags & IOS_F_RELU_PRE)) return 0;
   if (!tap_tma_enabled()) return 0;
   if (kh == 1 && kw == 1 && sh == 1 && sw == 1 && ph == 0 && pw == 0) return 0;
   if (sh > 8 || sw > 8) return 0;
@@ -850,9 +842,8 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
         p.fd_tilh = make_fastdiv((uint32_t)p.tiles_h);
       }
       // A via TMA when it is a plain [M, C] matrix: 1x1, stride 1, no padding, no pre-ReLU
-      // (pre-ReLU convs too: the producers apply the ReLU in smem after the TMA lands)
-      p.a_tma = (g.math != IOS_MATH_FP32_SIMT && !p.fdw && p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 &&
-                 p.pw == 0 && (!(p.flags & IOS_F_RELU_PRE) || relu_tma_enabled())) ? 1 : 0;
+      p.a_tma = (g.math != IOS_MATH_FP32_SIMT && !p.fdw && p.kh == 1 && p.kw == 1 && p.sh == 1 && p.sw == 1 && p.ph == 0 && p.pw == 0 &&
+                 !(p.flags & IOS_F_RELU_PRE)) ? 1 : 0;
       p.swap_ab = s.swap;
       p.BN = s.BN;
       p.n_tiles_n = s.ntn;

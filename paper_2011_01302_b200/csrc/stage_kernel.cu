@@ -951,7 +951,6 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
   uint64_t* hbar = bars + 16;                               // [2] halo + depthwise weights landed (halo path)
-  uint64_t* abar = bars + 20;                               // [kStages] TMA activation landed (pre-ReLU TMA)
   float* sbias_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // 2 x kMaxBN
   uint8_t* sdesc = reinterpret_cast<uint8_t*>(bars) + kBarBytes + kBiasBytes;           // kDescBytes
   uint8_t* sepi = sdesc + kDescBytes;                                                     // kEpiBytes: 4 x 4 KB
@@ -1013,7 +1012,6 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     }
     mbar_init(smem_u32(&hbar[0]), 1);
     mbar_init(smem_u32(&hbar[1]), 1);
-    for (int s = 0; s < kStages; ++s) mbar_init(smem_u32(&abar[s]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp && sd.has_gemm && DT != ET_F32X) {
@@ -1173,11 +1171,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // Tap TMA (P.tt): chunk c = (tap, channel block); ONE 4D tensor TMA brings that tap's input
         // pixels of the tile's output patch (element strides = conv strides; padding and channels
         // past C are out-of-bounds zeros) in the same 128 B-swizzled [row][128 B] layout.
-        // pre-ReLU convs (NASNet ReLU-conv units) take the same TMA loads: the activation lands on
-        // its own barrier (abar), all four producer warps apply the ReLU in place (elementwise, so
-        // the swizzle does not matter; padding zeros stay zero), then arrive on the full barrier
-        const bool trelu = (P.flags & 2) != 0;
-        if (warp == 0 || trelu) {
+        if (warp == 0) {
           const uint64_t tmap = P.tmap_a;
           const bool swap = P.swap_ab != 0;
           // weights: BN rows of tile nt into the B slot, or (swap-AB) 128 rows of tile mt into A
@@ -1205,51 +1199,26 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           }
           for (int c = c0; c < c1; ++c) {
             mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
-            if (warp == 0 && lane == 0) {
+            if (lane == 0) {
               const uint32_t fb = smem_u32(&full[ring.slot]);
-              const uint32_t xb = trelu ? smem_u32(&abar[ring.slot]) : fb;
-              mbar_arrive_expect_tx(fb, (trelu ? 0u : xbytes) + bbytes);
-              if (trelu) mbar_arrive_expect_tx(xb, xbytes);
+              mbar_arrive_expect_tx(fb, xbytes + bbytes);
               if (P.tt) {
                 const int tap = fdiv(P.fd_kblk, c);
                 const int cb = c - tap * kblk;
                 const int ti = fdiv(P.fd_kw, tap);
                 const int tj = tap - ti * kwid;
-                tma_load_4d(smem_u32(xbuf + ring.slot * xsb), tmap, cb * ELEMS, iw0 + tj, ih0 + ti, tn0, xb);
+                tma_load_4d(smem_u32(xbuf + ring.slot * xsb), tmap, cb * ELEMS, iw0 + tj, ih0 + ti, tn0, fb);
               } else {
-                tma_load_2d(smem_u32(xbuf + ring.slot * xsb), tmap, c * ELEMS, xrow0, xb);
+                tma_load_2d(smem_u32(xbuf + ring.slot * xsb), tmap, c * ELEMS, xrow0, fb);
               }
               bulk_g2s(smem_u32(wbuf + ring.slot * wsb), wsrc + c * wstep, bbytes, fb);
-              if (!trelu) mbar_arrive_cnt(fb, kProducerWarps);   // stands in for the 4 producer warps' arrivals
+              mbar_arrive_cnt(fb, kProducerWarps);   // stands in for the 4 producer warps' arrivals
               if (tfirst && c - c0 < 3) IOS_TRACE(c == c0 ? 2 : 8 + c - c0);
-            }
-            if (trelu) {
-              mbar_wait(smem_u32(&abar[ring.slot]), ring.phase);
-              const uint32_t xa = smem_u32(xbuf + ring.slot * xsb);
-              for (uint32_t o = (uint32_t)ptid * 16u; o < xbytes; o += 128u * 16u) {
-                uint32_t w[4];
-                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(xa + o));
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  if (ESZ == 4) {
-                    w[q] = __float_as_uint(fmaxf(__uint_as_float(w[q]), 0.f));
-                  } else {
-                    __nv_bfloat162 hb = *reinterpret_cast<__nv_bfloat162*>(&w[q]);
-                    hb = __hmax2(hb, __floats2bfloat162_rn(0.f, 0.f));
-                    w[q] = *reinterpret_cast<uint32_t*>(&hb);
-                  }
-                }
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(xa + o), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
-                             : "memory");
-              }
-              fence_proxy_async();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(smem_u32(&full[ring.slot]));   // one arrival per producer warp
             }
             __syncwarp();
             ring.next();
           }
-          if (warp == 0 && lane == 0 && tfirst) IOS_TRACE(12);
+          if (lane == 0 && tfirst) IOS_TRACE(12);
           tfirst = false;
         } else {
           ring.advance(c1 - c0);
