@@ -1,5 +1,6 @@
 #!/bin/bash
-# round-end measurement batch (scratch; results copied into profiles/ by hand). Latency caches go
+# round-end measurement batch: tests, smoke, bench of every config, ncu launch list + one --set full
+# capture (results copied into profiles/ by hand). Latency caches go
 # to /tmp on the box: gpurun_out is capped at 64 MiB.
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/final_gpu_tests.log 2>&1; tail -1 gpurun_out/final_gpu_tests.log
