@@ -169,6 +169,13 @@ def run_ours(args):
     search_s = time.time() - t0
     q_seq = g.schedule_sequential()
     q_greedy = g.schedule_greedy()
+    tune_s = 0.0
+    if args.tune:
+        # per-stage tiling variant by measurement, for every schedule alike (same kernels)
+        t1 = time.time()
+        for q in (q_ios, q_seq, q_greedy):
+            g.tune(q)
+        tune_s = time.time() - t1
 
     x = torch.from_numpy(net.make_input()).to(dev)
     out = torch.empty(g.output_shape(), dtype=torch.float32, device=dev)
@@ -273,6 +280,7 @@ def run_ours(args):
             "speedup_vs_greedy": round(ms_greedy / ms_ios, 3),
             "images_per_s": round(images * 1000.0 / ms_ios, 1),
             "search_s": round(search_s, 2),
+            "tune_s": round(tune_s, 2),
             "search_stats": {"states": q_ios.stats[0], "transitions": q_ios.stats[1], "stages_measured": q_ios.stats[2]},
             "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": unit,
                          "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -358,6 +366,7 @@ def main():
     ap.add_argument("--s", type=int, default=8)
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--latency-cache", default="", help="load (if present) / save the DP's stage-latency cache")
+    ap.add_argument("--tune", type=int, default=1, help="1: ios_schedule_tune every schedule (per-stage tiling), 0: default tiling")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -167,6 +167,14 @@ IOS_API ios_status ios_schedule_num_stages(ios_schedule q, int32_t* n);
 IOS_API ios_status ios_schedule_stage(ios_schedule q, int32_t i, int32_t* ops, int32_t cap, int32_t* n_ops,
                               ios_strategy* t, double* latency_ms);
 
+/* Stage tuner (an extension beyond the paper: the tile decomposition of each stage, not the
+ * schedule). Every stage of Q is measured on the device under each of the library's tiling
+ * variants (split-K granularity) with the ios_stage_latency protocol (`trials` x a CUDA graph of
+ * `reps` back-to-back launches, median; <= 0 = defaults 3 and 10) and later runs of ANY schedule
+ * use the fastest variant for that stage. Does not change Q or its outputs beyond floating-point
+ * summation order. Synchronises. Errors: IOS_ERR_INVALID_ARG, IOS_ERR_CUDA, IOS_ERR_KERNEL. */
+IOS_API ios_status ios_schedule_tune(ios_graph g, ios_schedule q, int32_t trials, int32_t reps);
+
 /* ---- execution ------------------------------------------------------------------------------ */
 
 /* Runs Q on `d_input` (device, caller-owned, NCHW fp32 [batch, c, h, w] contiguous) and writes the

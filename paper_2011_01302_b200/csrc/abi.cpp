@@ -405,6 +405,15 @@ ios_status ios_schedule_stage(ios_schedule qh, int32_t i, int32_t* ops, int32_t 
   ABI_END
 }
 
+ios_status ios_schedule_tune(ios_graph gh, ios_schedule qh, int32_t trials, int32_t reps) {
+  ABI_BEGIN
+  REQUIRE(gh && qh, "bad arguments");
+  REQUIRE(qh->q.g == &gh->g, "schedule belongs to another graph");
+  validate_schedule(gh->g, qh->q);
+  tune_schedule(gh->g, qh->q, trials > 0 ? trials : 3, reps > 0 ? reps : 10);
+  ABI_END
+}
+
 ios_status ios_run(ios_graph gh, ios_schedule qh, const void* d_in, void* d_out, void* stream) {
   ABI_BEGIN
   REQUIRE(gh && qh && d_in && d_out, "bad arguments");

@@ -62,6 +62,9 @@ struct DeviceState {
   void* l2buf = nullptr;
   int64_t l2bytes = 0;
   std::map<std::tuple<int, uint64_t, int>, StagePlan*> plans;
+  // per-stage tiling variant chosen by ios_schedule_tune (absent = 0, the default knobs)
+  std::map<std::tuple<int, uint64_t, int>, int> tile_variant;
+  std::vector<StagePlan*> retired;   // plans replaced by tuning (a captured schedule may use them)
 };
 
 namespace {
@@ -446,8 +449,14 @@ static TileKnobs tile_knobs() {
   return k;
 }
 
-void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms) {
-  const TileKnobs kn = tile_knobs();
+// Tiling variants the stage tuner (ios_schedule_tune) may pick per stage: 0 = the default knobs,
+// 1 = finer split-K (>= 2 chunks per unit), 2 = coarser split-K (>= 8 chunks per unit). Measured:
+// the best split-K granularity differs by network and stage (profiles/r1_kernel_ab_findings.md §5).
+constexpr int kTileVariants = 3;
+void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms, int variant = 0) {
+  TileKnobs kn = tile_knobs();
+  if (variant == 1) kn.min_cps = std::max(1, kn.min_cps / 2);
+  if (variant == 2) kn.min_cps = kn.min_cps * 2;
   const int target = kn.target_units > 0 ? kn.target_units : num_sms;
   for (GemmSpec* p : gs) {
     if (p->swap) {
@@ -642,8 +651,12 @@ void free_plan(DeviceState& d, StagePlan* p) {
   delete p;
 }
 
-StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
+StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int variant = -1) {
   DeviceState& d = *g.dev;
+  if (variant < 0) {
+    auto vit = d.tile_variant.find(std::make_tuple(bpos, mask, strategy));
+    variant = vit == d.tile_variant.end() ? 0 : vit->second;
+  }
   const std::vector<int> ops = g.ops_of(bpos, mask);
   PlanBuilder b(g);
   auto* plan = new StagePlan();
@@ -820,7 +833,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy) {
     std::vector<GemmSpec*> gs;
     for (size_t i = 0; i < b.probs.size(); ++i)
       if (b.probs[i].kind == PK_GEMM) gs.push_back(&b.specs[i]);
-    choose_tiling(gs, simt_tiles, d.num_sms);
+    choose_tiling(gs, simt_tiles, d.num_sms, variant);
     size_t ws_bytes = 0;
     int n_tilectr = 0;
     for (size_t i = 0; i < b.probs.size(); ++i) {
@@ -1039,6 +1052,65 @@ GraphExec capture(DeviceState& d, F&& body) {
   return g;
 }
 }  // namespace
+
+// Stage tuner: every stage of Q is measured under each tiling variant (the profiler protocol of
+// ios_stage_latency: warm-up, trials x CUDA-graph reps, median) and keeps the fastest. Stages
+// shared by several schedules get one choice. Plans already built with another variant are
+// retired (freed with the graph), so schedules captured earlier stay valid.
+void tune_schedule(Graph& g, Schedule& q, int trials, int reps) {
+  ensure_device(g);
+  DeviceState& d = *g.dev;
+  for (const Stage& st : q.stages) {
+    int bpos = -1;
+    const uint64_t mask = g.mask_of(st.ops, &bpos);
+    const auto pk = std::make_tuple(bpos, mask, st.strategy);
+    if (d.tile_variant.count(pk)) continue;   // tuned for an earlier schedule
+    double best = kInf;
+    int best_v = 0;
+    for (int v = 0; v < kTileVariants; ++v) {
+      StagePlan* p = nullptr;
+      try {
+        p = build_plan(g, bpos, mask, st.strategy, v);
+      } catch (const Error& e) {
+        if (e.code != IOS_ERR_UNSUPPORTED) throw;
+        continue;
+      }
+      double ms = 0.0;
+      if (!p->empty) {
+        for (int i = 0; i < 3; ++i) launch_plan(p, d.stream);
+        GraphExec rep = capture(d, [&] {
+          for (int i = 0; i < reps; ++i) launch_plan(p, d.stream);
+        });
+        std::vector<double> t;
+        for (int tr = 0; tr < trials; ++tr) {
+          IOS_CHECK_CUDA(cudaEventRecord(d.ev0, d.stream));
+          IOS_CHECK_CUDA(cudaGraphLaunch(rep.exec, d.stream));
+          IOS_CHECK_CUDA(cudaEventRecord(d.ev1, d.stream));
+          IOS_CHECK_CUDA(cudaEventSynchronize(d.ev1));
+          float e = 0;
+          IOS_CHECK_CUDA(cudaEventElapsedTime(&e, d.ev0, d.ev1));
+          t.push_back((double)e / reps);
+        }
+        check_err(d);
+        std::sort(t.begin(), t.end());
+        ms = t[t.size() / 2];
+      }
+      IOS_CHECK_CUDA(cudaStreamSynchronize(d.stream));
+      free_plan(d, p);
+      if (ms < best) {
+        best = ms;
+        best_v = v;
+      }
+    }
+    d.tile_variant[pk] = best_v;
+    auto it = d.plans.find(pk);
+    if (it != d.plans.end()) {   // rebuilt with the chosen variant on next use
+      d.retired.push_back(it->second);
+      d.plans.erase(it);
+    }
+  }
+  destroy_schedule_exec(q);
+}
 
 double stage_latency(Graph& g, const std::vector<int>& ops, int strategy, const ios_profile_opts* opts) {
   ensure_device(g);
@@ -1274,6 +1346,7 @@ void destroy_device(Graph& g) {
   if (!g.dev) return;
   DeviceState& d = *g.dev;
   for (auto& [k, p] : d.plans) free_plan(d, p);
+  for (StagePlan* p : d.retired) free_plan(d, p);
   if (d.stream) cudaStreamSynchronize(d.stream);
   for (void* p : d.allocs) cudaFree(p);
   if (d.ev0) cudaEventDestroy(d.ev0);

@@ -110,6 +110,7 @@ void op_output(Graph& g, int op, void* d_out, cudaStream_t st);
 int schedule_launches(Graph& g, Schedule& q);
 int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* out, int cap);
 void destroy_device(Graph& g);
+void tune_schedule(Graph& g, Schedule& q, int trials, int reps);
 void destroy_schedule_exec(Schedule& q);
 
 // kernels (stage_kernel.cu)

@@ -73,6 +73,7 @@ def _load():
         "ios_schedule_create": [P, I32, pI32, pI32, pI32, C.POINTER(P)],
         "ios_schedule_num_stages": [P, pI32],
         "ios_schedule_stage": [P, I32, pI32, I32, pI32, pI32, pD],
+        "ios_schedule_tune": [P, P, I32, I32],
         "ios_run": [P, P, P, P, P],
         "ios_run_host": [P, P, C.POINTER(C.c_float), C.POINTER(C.c_float), P],
         "ios_op_output": [P, I32, P, P],
@@ -152,6 +153,10 @@ def ios_schedule_dp(g, r: int, s: int, cost: Optional[Callable[[int, int, int], 
     stats = (C.c_int64 * 3)()
     _check(lib.ios_schedule_dp_ex(g, r, s, STRATEGY_SETS[strategies], cb, None, C.byref(q), C.byref(tot), stats))
     return q, tot.value, tuple(int(v) for v in stats)
+
+
+def ios_schedule_tune(g, q, trials: int = 0, reps: int = 0) -> None:
+    _check(lib.ios_schedule_tune(g, q, trials, reps))
 
 
 def ios_run(g, q, d_input: int, d_output: int, stream: int = 0) -> None:
@@ -257,6 +262,10 @@ class Graph:
     def schedule_dp(self, r: int = 3, s: int = 8, cost=None, strategies: str = "both") -> Schedule:
         q, c, stats = ios_schedule_dp(self.handle, r, s, cost, strategies)
         return Schedule(self, q, c, stats)
+
+    def tune(self, q: Schedule, trials: int = 0, reps: int = 0) -> None:
+        """ios_schedule_tune: pick each stage's tiling variant by measurement (call before runs)."""
+        ios_schedule_tune(self.handle, q.handle, trials, reps)
 
     def schedule_sequential(self) -> Schedule:
         q = C.c_void_p()

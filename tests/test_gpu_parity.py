@@ -184,3 +184,19 @@ print(len(set(hs)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip().splitlines()[-1] == "1", out.stdout
+
+
+def test_tuned_schedule_parity(torch_cuda):
+    """ios_schedule_tune re-tiles stages (split-K granularity) by measurement: the outputs still
+    match the oracle per op, for the sequential and greedy schedules of the conv zoo."""
+    from paper_2011_01302_b200 import Graph
+    net = W.build("conv_zoo", batch=1, hw=37, math="tf32")
+    g = Graph.from_netspec(net, "tf32")
+    x = torch_cuda.from_numpy(net.make_input()).cuda()
+    for q in (g.schedule_sequential(), g.schedule_greedy()):
+        g.tune(q)
+        g.run(q, x)
+        torch_cuda.cuda.synchronize()
+        errs = per_op_errors(net, g, "tf32")
+        worst = max(errs, key=errs.get)
+        assert errs[worst] < TOL["tf32"], (worst, net.op(worst).name, errs[worst])
