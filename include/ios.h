@@ -180,10 +180,17 @@ IOS_API ios_status ios_schedule_tune(ios_graph g, ios_schedule q, int32_t trials
 /* Runs Q on `d_input` (device, caller-owned, NCHW fp32 [batch, c, h, w] contiguous) and writes the
  * last op's output to `d_output` (device, caller-owned, NCHW fp32 contiguous). Stream-ordered and
  * asynchronous on `cuda_stream` (a cudaStream_t; NULL = legacy default stream). The first call for
- * a schedule builds its stage plans and captures them into a CUDA graph. */
+ * a schedule builds its stage plans and captures them into a CUDA graph (re-captured after
+ * ios_schedule_tune replaced a plan). IOS_ERR_KERNEL: a dependency wait of an EARLIER run on this
+ * graph timed out (the flag is host-mapped and read at the next call; see ios_sync). */
 IOS_API ios_status ios_run(ios_graph g, ios_schedule q, const void* d_input, void* d_output, void* cuda_stream);
-/* Same with HOST buffers: copies the input in, runs, copies the output back, synchronises. */
+/* Same with HOST buffers: copies the input in, runs, copies the output back, synchronises.
+ * IOS_ERR_KERNEL if an in-kernel dependency wait of this run timed out (outputs invalid). */
 IOS_API ios_status ios_run_host(ios_graph g, ios_schedule q, const float* h_input, float* h_output, void* cuda_stream);
+/* Synchronises `cuda_stream` (and the library's own stream) and reports IOS_ERR_KERNEL if an
+ * in-kernel dependency wait of any earlier run on this graph timed out (the ~4 s deadlock guard:
+ * the outputs of that run are invalid). ios_run itself reports such a flag at its next call. */
+IOS_API ios_status ios_sync(ios_graph g, void* cuda_stream);
 /* Copies op `op`'s most recent output (NCHW fp32) to caller-owned device memory. */
 IOS_API ios_status ios_op_output(ios_graph g, int32_t op, void* d_out, void* cuda_stream);
 /* Number of kernel launches one ios_run of q performs (stage kernels + boundary layout kernels). */
@@ -203,6 +210,8 @@ IOS_API ios_status ios_latency_cache_load(ios_graph g, const char* path);
 IOS_API ios_status ios_latency_cache_autosave(ios_graph g, const char* path);
 
 IOS_API const char* ios_last_error(void);
+/* Content hash of the sources this library was compiled from (build.py), for provenance checks. */
+IOS_API const char* ios_build_id(void);
 IOS_API void ios_schedule_destroy(ios_schedule q);
 IOS_API void ios_graph_destroy(ios_graph g);
 

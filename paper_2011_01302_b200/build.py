@@ -14,16 +14,34 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-cudart", "static", "--expt-relaxed-constexpr"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+ID_FILE = LIB + ".buildid"
+
+
+def source_hash() -> str:
+    """Content hash of everything libios.so is compiled from (sources, header, flags, this file).
+    It is compiled into the library (ios_build_id()) and stored beside it, so a stale or foreign
+    binary is rebuilt whatever the file times say, and tests can check the loaded .so is HEAD's."""
+    import hashlib
+    h = hashlib.sha256()
+    deps = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp", ".h")))
+    for p in deps + [os.path.join(HERE, "..", "include", "ios.h"), os.path.abspath(__file__)]:
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+def _stale(sid: str) -> bool:
+    if not os.path.exists(LIB) or not os.path.exists(ID_FILE):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "ios.h"), __file__]
-    return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
+    with open(ID_FILE) as f:
+        return f.read().strip() != sid
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+    sid = source_hash()
+    if not force and not _stale(sid):
         return LIB
     objs = []
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
@@ -35,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src, defs in units:
         tag = "".join(d.split("=")[1] for d in defs)
         obj = os.path.join(HERE, "build", src + (f".inst{tag}" if tag else "") + ".o")
-        cmd = [NVCC, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *defs, f'-DIOS_BUILD_ID="{sid}"', "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu") and verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -54,6 +72,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, *FLAGS, "-shared", "-o", tmp, *objs]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    with open(ID_FILE, "w") as f:
+        f.write(sid + "\n")
     return LIB
 
 

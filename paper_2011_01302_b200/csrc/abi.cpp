@@ -443,9 +443,21 @@ ios_status ios_run_host(ios_graph gh, ios_schedule qh, const float* h_in, float*
   IOS_CHECK_CUDA(cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st));
   IOS_CHECK_CUDA(cudaFreeAsync(d_in, st));
   IOS_CHECK_CUDA(cudaFreeAsync(d_out, st));
-  IOS_CHECK_CUDA(cudaStreamSynchronize(st));
+  sync_and_check(g, st);   // IOS_ERR_KERNEL if a dependency wait of this run timed out
   ABI_END
 }
+
+ios_status ios_sync(ios_graph gh, void* stream) {
+  ABI_BEGIN
+  REQUIRE(gh, "bad arguments");
+  sync_and_check(gh->g, reinterpret_cast<cudaStream_t>(stream));
+  ABI_END
+}
+
+#ifndef IOS_BUILD_ID
+#define IOS_BUILD_ID "unknown"
+#endif
+const char* ios_build_id(void) { return IOS_BUILD_ID; }
 
 ios_status ios_op_output(ios_graph gh, int32_t op, void* d_out, void* stream) {
   ABI_BEGIN
@@ -487,8 +499,14 @@ void save_latency_cache(const Graph& g, const std::string& path) {
     if (!f) IOS_FAIL(IOS_ERR_INVALID_ARG, "cannot write " + path);
     f << graph_signature(g) << "\n";
     f.precision(17);
-    for (auto& [k, v] : g.latency_cache)
-      f << std::get<0>(k) << " " << std::get<1>(k) << " " << std::get<2>(k) << " " << v << "\n";
+    // an unsupported stage is cached as inf: written as the token "inf" (istream >> double cannot
+    // parse it; the loader reads tokens and converts with strtod, which can)
+    for (auto& [k, v] : g.latency_cache) {
+      f << std::get<0>(k) << " " << std::get<1>(k) << " " << std::get<2>(k) << " ";
+      if (std::isinf(v)) f << "inf";
+      else f << v;
+      f << "\n";
+    }
   }
   std::rename(tmp.c_str(), path.c_str());
 }
@@ -518,10 +536,22 @@ ios_status ios_latency_cache_load(ios_graph gh, const char* path) {
   std::string sig;
   std::getline(f, sig);
   if (sig != graph_signature(gh->g)) IOS_FAIL(IOS_ERR_INVALID_ARG, "latency cache belongs to another graph");
-  unsigned long long bsig, m;
-  int t;
-  double v;
-  while (f >> bsig >> m >> t >> v) gh->g.latency_cache[std::make_tuple((uint64_t)bsig, (uint64_t)m, t)] = v;
+  std::string a, b, c, d;
+  int line = 1;
+  while (f >> a) {
+    ++line;
+    if (!(f >> b >> c >> d)) IOS_FAIL(IOS_ERR_INVALID_ARG, std::string(path) + ": truncated entry at line " + std::to_string(line));
+    char* e1 = nullptr;
+    char* e2 = nullptr;
+    char* e3 = nullptr;
+    char* e4 = nullptr;
+    const unsigned long long bsig = std::strtoull(a.c_str(), &e1, 10), m = std::strtoull(b.c_str(), &e2, 10);
+    const long t = std::strtol(c.c_str(), &e3, 10);
+    const double v = std::strtod(d.c_str(), &e4);
+    if (*e1 || *e2 || *e3 || *e4 || (t != IOS_CONCURRENT && t != IOS_MERGE))
+      IOS_FAIL(IOS_ERR_INVALID_ARG, std::string(path) + ": malformed entry at line " + std::to_string(line));
+    gh->g.latency_cache[std::make_tuple((uint64_t)bsig, (uint64_t)m, (int)t)] = v;
+  }
   ABI_END
 }
 

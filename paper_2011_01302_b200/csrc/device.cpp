@@ -58,13 +58,14 @@ struct DeviceState {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<OpDev> od;
   std::vector<void*> allocs;
-  int* err = nullptr;
+  int* err = nullptr;                // kernel error flag: pinned, host-mapped (read without a copy)
   void* l2buf = nullptr;
   int64_t l2bytes = 0;
   std::map<std::tuple<int, uint64_t, int>, StagePlan*> plans;
   // per-stage tiling variant chosen by ios_schedule_tune (absent = 0, the default knobs)
   std::map<std::tuple<int, uint64_t, int>, int> tile_variant;
   std::vector<StagePlan*> retired;   // plans replaced by tuning (a captured schedule may use them)
+  uint64_t plan_gen = 0;             // bumped when tuning replaces plans: captured schedules re-capture
 };
 
 namespace {
@@ -240,7 +241,18 @@ void ensure_device(Graph& g) {
   }
   IOS_CHECK_CUDA(cudaEventCreate(&d.ev0));
   IOS_CHECK_CUDA(cudaEventCreate(&d.ev1));
-  d.err = static_cast<int*>(dmalloc(d, 16));
+  {
+    void* p = nullptr;
+    IOS_CHECK_CUDA(cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(p, 0, 64);
+    void* dp = nullptr;
+    IOS_CHECK_CUDA(cudaHostGetDevicePointer(&dp, p, 0));
+    if (dp != p) {
+      cudaFreeHost(p);
+      IOS_FAIL(IOS_ERR_CUDA, "host-mapped error flag needs unified addressing");
+    }
+    d.err = static_cast<int*>(p);
+  }
   d.l2bytes = 2 * (int64_t)prop.l2CacheSize;
 
   const int n = (int)g.ops.size();
@@ -882,16 +894,16 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       p.tile_begin = tiles;
       tiles += p.n_tiles;
     }
-    const int n_counters = 1 + np + n_tilectr;
+    const int n_counters = kCounterBase + np + n_tilectr;
     for (int i = 0; i < np; ++i) {
       Problem& p = b.probs[i];
-      p.done_idx = 1 + i;
+      p.done_idx = kCounterBase + i;
       for (int k = 0; k < p.n_deps; ++k) {
         const Problem& q = b.probs[p.dep_idx[k]];
         p.dep_target[k] = q.n_tiles;   // every unit (incl. each split-K part) signals once
-        p.dep_idx[k] = 1 + p.dep_idx[k];
+        p.dep_idx[k] = kCounterBase + p.dep_idx[k];
       }
-      if (p.kind == PK_GEMM && p.split > 1) p.tilectr_idx += 1 + np;
+      if (p.kind == PK_GEMM && p.split > 1) p.tilectr_idx += kCounterBase + np;
     }
     plan->empty = tiles == 0;
     if (!plan->empty) {
@@ -902,7 +914,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
                    sb = b.segs.size() * sizeof(Segment);
       // a problem signals completion only if a later member of the stage waits on it
       for (Problem& p : b.probs)
-        for (int k = 0; k < p.n_deps; ++k) b.probs[p.dep_idx[k] - 1].signal = 1;
+        for (int k = 0; k < p.n_deps; ++k) b.probs[p.dep_idx[k] - kCounterBase].signal = 1;
       std::vector<uint8_t> blob(pb + vb + sb + 64, 0);
       std::memcpy(blob.data(), b.probs.data(), pb);
       if (vb) std::memcpy(blob.data() + pb, b.views.data(), vb);
@@ -1011,16 +1023,27 @@ void launch_plan(const StagePlan* p, cudaStream_t st) {
   IOS_CHECK_CUDA(launch_stage(p->sd, p->dtype, p->grid, st));
 }
 
+}  // namespace
+
+// The kernel's error flag lives in host-mapped pinned memory: reading it needs no copy and no
+// synchronisation. Callers read it after a synchronisation (profiler, tuner, ios_run_host, ios_sync)
+// or, in ios_run, at the next call (a flag set by any earlier, completed launch is reported then).
 void check_err(DeviceState& d) {
-  int h = 0;
-  IOS_CHECK_CUDA(cudaMemcpy(&h, d.err, sizeof(int), cudaMemcpyDeviceToHost));
-  if (h) {
-    IOS_CHECK_CUDA(cudaMemset(d.err, 0, sizeof(int)));
-    IOS_FAIL(IOS_ERR_KERNEL, "in-kernel dependency wait timed out");
+  if (!d.err) return;
+  volatile int* f = d.err;
+  if (*f) {
+    *f = 0;
+    IOS_FAIL(IOS_ERR_KERNEL, "in-kernel dependency wait timed out (a stage's CTAs were not co-resident, or a "
+                             "producer never signalled); outputs of that run are invalid");
   }
 }
 
-}  // namespace
+void sync_and_check(Graph& g, cudaStream_t st) {
+  if (!g.dev || !g.dev->ready) return;
+  IOS_CHECK_CUDA(cudaStreamSynchronize(st));
+  IOS_CHECK_CUDA(cudaStreamSynchronize(g.dev->stream));
+  check_err(*g.dev);
+}
 
 namespace {
 // A stream-captured CUDA graph (owned; destroyed with the object).
@@ -1107,6 +1130,7 @@ void tune_schedule(Graph& g, Schedule& q, int trials, int reps) {
     if (it != d.plans.end()) {   // rebuilt with the chosen variant on next use
       d.retired.push_back(it->second);
       d.plans.erase(it);
+      ++d.plan_gen;              // every captured schedule re-captures with the new plan
     }
   }
   destroy_schedule_exec(q);
@@ -1278,7 +1302,8 @@ int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* o
 void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStream_t st) {
   ensure_device(g);
   DeviceState& d = *g.dev;
-  if (!q.exec || q.exec_in != d_in || q.exec_out != d_out) {
+  check_err(d);   // a dependency-wait timeout in an earlier (completed) run
+  if (!q.exec || q.exec_in != d_in || q.exec_out != d_out || q.exec_gen != d.plan_gen) {
     destroy_schedule_exec(q);
     std::vector<StagePlan*> plans;
     for (const Stage& s : q.stages) {
@@ -1286,6 +1311,9 @@ void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStre
       const uint64_t mask = g.mask_of(s.ops, &bpos);
       plans.push_back(get_plan(g, bpos, mask, s.strategy));
     }
+    // plans are built on the library's stream (pool allocations, descriptor / weight / tensor-map
+    // uploads, counter memsets): they must be complete before the caller's stream runs them
+    IOS_CHECK_CUDA(cudaStreamSynchronize(d.stream));
     const Op& in = g.ops[0];
     const Op& last = g.ops.back();
     IOS_CHECK_CUDA(cudaStreamBeginCapture(d.stream, cudaStreamCaptureModeThreadLocal));
@@ -1313,6 +1341,7 @@ void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStre
     IOS_CHECK_CUDA(cudaGraphInstantiate(&q.exec, graph, 0));
     q.exec_in = d_in;
     q.exec_out = d_out;
+    q.exec_gen = d.plan_gen;
     q.n_launches = launches;
   }
   IOS_CHECK_CUDA(cudaGraphLaunch(q.exec, st));
@@ -1345,10 +1374,12 @@ void destroy_schedule_exec(Schedule& q) {
 void destroy_device(Graph& g) {
   if (!g.dev) return;
   DeviceState& d = *g.dev;
+  if (d.ready) cudaDeviceSynchronize();   // callers' streams may still run this graph's stages
   for (auto& [k, p] : d.plans) free_plan(d, p);
   for (StagePlan* p : d.retired) free_plan(d, p);
   if (d.stream) cudaStreamSynchronize(d.stream);
   for (void* p : d.allocs) cudaFree(p);
+  if (d.err) cudaFreeHost(d.err);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
   if (d.stream) cudaStreamDestroy(d.stream);

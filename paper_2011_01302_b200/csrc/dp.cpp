@@ -35,10 +35,14 @@ class BlockDP {
     const int n = (int)b_.ops.size();
     const uint64_t v = n == 64 ? ~0ull : ((1ull << n) - 1);
     const double total = scheduler(v);                       // L5
+    // every ending costed inf (an infinite/NaN cost callback, or stages the device cannot run):
+    // no finite schedule exists, and L8-11 would find no choice to peel
+    if (!(total < kInf)) IOS_FAIL(IOS_ERR_UNSUPPORTED, "no finite-cost schedule for block " + std::to_string(b_.id));
     q->clear();                                              // L6
     uint64_t s = v;                                          // L7
     while (s) {                                              // L8
       const Memo& m = memo_.at(s);                           // L9
+      if (!m.choice) IOS_FAIL(IOS_ERR_UNSUPPORTED, "no finite-cost schedule for block " + std::to_string(b_.id));
       q->insert(q->begin(), {m.choice, m.strategy});         // L10
       s &= ~m.choice;                                        // L11
     }

@@ -94,6 +94,7 @@ struct Schedule {
   const void* exec_in = nullptr;
   void* exec_out = nullptr;
   cudaStream_t exec_stream = nullptr;
+  uint64_t exec_gen = 0;   // DeviceState::plan_gen the exec was captured with
   int n_launches = -1;
   ~Schedule();
 };
@@ -112,6 +113,7 @@ int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* o
 void destroy_device(Graph& g);
 void tune_schedule(Graph& g, Schedule& q, int trials, int reps);
 void destroy_schedule_exec(Schedule& q);
+void sync_and_check(Graph& g, cudaStream_t st);   // synchronise, then IOS_ERR_KERNEL if a wait timed out
 
 // kernels (stage_kernel.cu)
 cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t st);

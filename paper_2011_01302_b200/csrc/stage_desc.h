@@ -25,6 +25,7 @@ constexpr int kMmaWarp = 8;               // warp 8: tcgen05.mma issuer + TMEM a
 constexpr int kThreads = 9 * 32;
 constexpr int kTmemCols = 512;            // 2 accumulator buffers x 256 columns
 constexpr int kMaxProblems = 96;
+constexpr int kCounterBase = 2;       // counters[0..1]: the 64-bit launch counter
 constexpr int kSlabSplits = 1;            // split-K: problems with <= this many splits store per-split
                                           // slabs summed in split order (deterministic); the others reduce
                                           // into one zeroed slab (red.add: measured faster at every split
@@ -134,14 +135,15 @@ struct StageDesc {
   uint64_t problems;                // Problem[n_problems]
   uint64_t views;                   // View[]
   uint64_t segs;                    // Segment[]
-  uint64_t counters;                // int32[n_counters]; [0] = launch epoch (see uses_counters)
-  uint64_t err;                     // int32 error flag (dependency-wait timeout)
+  uint64_t counters;                // int32[n_counters]; [0..1] = 64-bit launch counter (see uses_counters)
+  uint64_t err;                     // int32 error flag (dependency-wait timeout), host-mapped pinned memory
   uint64_t trace;                   // optional uint64 [grid][16] timeline (0 = off)
   int32_t n_problems, n_tiles, n_counters, has_gemm;
   int32_t blob_bytes;               // problems | views | segments, contiguous from `problems`
   int32_t views_off, segs_off;
-  int32_t uses_counters;            // any in-stage dependency or split-K: counters[0] is the launch
-                                    // epoch, the others grow monotonically (targets epoch-relative)
+  int32_t uses_counters;            // any in-stage dependency or split-K: counters[0..1] count launches
+                                    // (epoch), the others grow monotonically (targets epoch-relative,
+                                    // compared wrap-safely mod 2^32)
   int32_t ring_slots;               // smem ring depth this launch: kStages, or kStages - 1 when a halo
                                     // problem borrows the last slot
 };

@@ -21,6 +21,7 @@
 #include <stdint.h>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "stage_desc.h"
 
@@ -289,17 +290,25 @@ __device__ __forceinline__ void store_elem(const View& vw, int dtype, int64_t pi
 
 // ------------------------------------------------------------------------------ dependency waits
 // Counters are never reset: every launch adds the same amounts, and launch number `ep` (the epoch,
-// derived at kernel start) turns the per-launch targets into absolute ones: wait until
-// counter >= (ep + 1) * target (int arithmetic; wraps only after ~10^7 launches of one plan).
-__device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* err, int ep) {
+// derived at kernel start from a 64-bit launch counter) turns the per-launch targets into absolute
+// ones: wait until counter >= (ep + 1) * target. Both sides are taken mod 2^32 and compared
+// wrap-safely ((int)(c - target) < 0): within one launch a counter is never more than one launch's
+// increment away from its target, so the difference always fits an int, for any number of launches.
+// A wait that exceeds ~4 s stores 1 into the error flag (host-mapped pinned memory: the host reads it
+// without a copy; IOS_ERR_KERNEL from the next ios_run / ios_run_host / ios_sync) and gives up.
+__device__ __forceinline__ bool before(int c, uint32_t target) { return (int)((uint32_t)c - target) < 0; }
+__device__ __forceinline__ void flag_error(int* err) {
+  asm volatile("st.volatile.global.s32 [%0], %1;" ::"l"(err), "r"(1) : "memory");
+}
+__device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* err, uint32_t ep) {
   for (int d = 0; d < P.n_deps; ++d) {
     const int* c = counters + P.dep_idx[d];
-    const int target = (ep + 1) * P.dep_target[d];
+    const uint32_t target = (ep + 1u) * (uint32_t)P.dep_target[d];
     long long t0 = clock64();
-    while (ld_acquire(c) < target) {
+    while (before(ld_acquire(c), target)) {
       __nanosleep(64);
       if (clock64() - t0 > (long long)8000000000LL) {   // ~4 s: deadlock guard -> IOS_ERR_KERNEL
-        atomicExch(err, 1);
+        flag_error(err);
         break;
       }
     }
@@ -309,14 +318,14 @@ __device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* 
 // split-K rendezvous: every split of an output tile arrives after its reductions, then waits for
 // all `n` (the splits of one tile run on distinct, co-resident CTAs; a tile's splits only wait for
 // tiles with higher indices, which the CTAs reach after finishing lower ones: no cycle)
-__device__ __forceinline__ void split_rendezvous(int* ctr, int n, int* err, int ep) {
+__device__ __forceinline__ void split_rendezvous(int* ctr, int n, int* err, uint32_t ep) {
   atom_acqrel_add(ctr, 1);
-  const int target = (ep + 1) * n;
+  const uint32_t target = (ep + 1u) * (uint32_t)n;
   long long t0 = clock64();
-  while (ld_acquire(ctr) < target) {
+  while (before(ld_acquire(ctr), target)) {
     __nanosleep(32);
     if (clock64() - t0 > (long long)8000000000LL) {
-      atomicExch(err, 1);
+      flag_error(err);
       break;
     }
   }
@@ -1045,12 +1054,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   // here on we read activations (and counters) the previous grid may still be writing
   if (tid == 0) IOS_TRACE(11);   // before waiting for the previous grid
   pdl_wait();
-  // launch epoch: every CTA of a launch adds 1 to counters[0] exactly once, before releasing the
+  // launch epoch: every CTA of a launch adds 1 to the launch counter exactly once, before releasing the
   // next launch (launch_dependents), so old / grid is this launch's number for every CTA
-  if (sd.uses_counters && tid == 0) *flag = atomicAdd(counters, 1) / (int)gridDim.x;
+  // (64-bit, in counters[0..1]: it never wraps; the epoch itself is used mod 2^32)
+  if (sd.uses_counters && tid == 0)
+    *flag = (int)(uint32_t)(atomicAdd(reinterpret_cast<unsigned long long*>(counters), 1ull) / gridDim.x);
   pdl_launch_dependents();
   named_bar(4, kThreads);
-  const int ep = sd.uses_counters ? *flag : 0;
+  const uint32_t ep = sd.uses_counters ? (uint32_t)*flag : 0u;
   if (tid == 0) IOS_TRACE(1);
 
   if (!sd.has_gemm) {
@@ -1915,12 +1926,21 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #define IOS_LAUNCHER_DECL(dt, sdv) cudaError_t launch_stage_inst_##dt##_##sdv(cudaLaunchConfig_t& cfg, const StageDesc& sd)
 IOS_LAUNCHER_DEF2(IOS_INST_DT, IOS_INST_SD) {
   static bool attr_done = false;
+  static int max_grid = 0;
   auto k = ios_stage_kernel<IOS_INST_DT, (IOS_INST_SD != 0)>;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
     if (e != cudaSuccess) return e;
+    // co-residency: the in-kernel dependency waits assume every CTA of the grid is resident at
+    // once (one per SM); refuse a grid the device cannot hold instead of spinning into the guard
+    int per_sm = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, kThreads, kSmemBytes + 1024);
+    if (e != cudaSuccess) return e;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    max_grid = per_sm * sms;
     attr_done = true;
   }
+  if ((int)(cfg.gridDim.x) > max_grid) return cudaErrorCooperativeLaunchTooLarge;
   return cudaLaunchKernelEx(&cfg, k, sd);
 }
 
@@ -1972,11 +1992,18 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes + 1024;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // IOS_COOP=1: cooperative launch (the runtime guarantees co-residency of the whole grid or fails)
+  static const bool coop = getenv("IOS_COOP") && atoi(getenv("IOS_COOP")) != 0;
+  if (coop) {
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.numAttrs = 2;
+  }
   const bool smem_desc = sd.blob_bytes <= kDescBytes;
   if (dtype == ET_BF16) return smem_desc ? launch_stage_inst_1_1(cfg, sd) : launch_stage_inst_1_0(cfg, sd);
   if (dtype == ET_F32X) return smem_desc ? launch_stage_inst_2_1(cfg, sd) : launch_stage_inst_2_0(cfg, sd);

@@ -81,6 +81,7 @@ def _load():
         "ios_latency_cache_save": [P, C.c_char_p],
         "ios_latency_cache_load": [P, C.c_char_p],
         "ios_latency_cache_autosave": [P, C.c_char_p],
+        "ios_sync": [P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -88,6 +89,8 @@ def _load():
         f.restype = I32
     lib.ios_last_error.restype = C.c_char_p
     lib.ios_last_error.argtypes = []
+    lib.ios_build_id.restype = C.c_char_p
+    lib.ios_build_id.argtypes = []
     lib.ios_schedule_destroy.argtypes = [P]
     lib.ios_schedule_destroy.restype = None
     lib.ios_graph_destroy.argtypes = [P]
@@ -165,6 +168,15 @@ def ios_run(g, q, d_input: int, d_output: int, stream: int = 0) -> None:
 
 def ios_last_error() -> str:
     return (lib.ios_last_error() or b"").decode()
+
+
+def ios_sync(g, stream: int = 0) -> None:
+    """Synchronise `stream`; IOS_ERR_KERNEL if an in-kernel dependency wait of an earlier run timed out."""
+    _check(lib.ios_sync(g, C.c_void_p(stream)))
+
+
+def ios_build_id() -> str:
+    return (lib.ios_build_id() or b"").decode()
 
 
 # ---------------------------------------------------------------------------- conveniences
@@ -304,6 +316,13 @@ class Graph:
         _check(lib.ios_run_host(self.handle, q.handle, x.ctypes.data_as(C.POINTER(C.c_float)),
                                 out.ctypes.data_as(C.POINTER(C.c_float)), None))
         return out
+
+    def sync(self, stream=None) -> None:
+        """ios_sync on `stream` (default: torch's current stream of the graph's device)."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(torch.device(f"cuda:{self.device}")).cuda_stream
+        ios_sync(self.handle, stream)
 
     def op_output(self, op: int, stream=None):
         import torch

@@ -179,3 +179,41 @@ def test_no_cpu_fallback_without_gpu(ios):
     with pytest.raises(ios.IOSError) as e:
         g.stage_latency([1])
     assert e.value.status == 8                                     # IOS_ERR_CUDA, never a CPU path
+
+
+def test_loaded_library_is_built_from_these_sources(ios):
+    """Provenance: the .so the tests load carries the content hash of the sources in this tree
+    (build.py compiles it in as ios_build_id()), so a stale or foreign binary cannot pass for HEAD."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_ios_build", os.path.join(ROOT, "paper_2011_01302_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert ios.ios.ios_build_id() == mod.source_hash()
+
+
+@pytest.mark.timeout(60)
+@pytest.mark.parametrize("bad", [math.inf, math.nan])
+def test_dp_all_infinite_costs_is_an_error_not_a_hang(ios, bad):
+    """Every ending costing inf/NaN leaves no finite schedule: the library reports it (the oracle
+    raises too) instead of looping in Algorithm 1's L8-11 reconstruction."""
+    g = ios.Graph.from_netspec(W.fig2_block())
+    with pytest.raises(ios.IOSError) as e:
+        g.schedule_dp(3, 8, lambda b, m, t: bad)
+    assert e.value.status == 11
+
+
+def test_latency_cache_keeps_entries_after_an_infinite_one(ios, tmp_path):
+    """An unsupported stage is cached as inf; it must round-trip and must not truncate the load."""
+    g = ios.Graph.from_netspec(W.fig2_block())
+    p = tmp_path / "cache.txt"
+    g.save_latency_cache(str(p))
+    sig = p.read_text().splitlines()[0]
+    p.write_text(sig + "\n7 1 0 inf\n7 2 0 0.0125\n7 13 1 0.03\n")
+    g.load_latency_cache(str(p))
+    p2 = tmp_path / "cache2.txt"
+    g.save_latency_cache(str(p2))
+    rows = sorted(l.split() for l in p2.read_text().splitlines()[1:])
+    assert rows == [["7", "1", "0", "inf"], ["7", "13", "1", "0.029999999999999999"], ["7", "2", "0", "0.012500000000000001"]]
+    p.write_text(sig + "\n7 1 0 abc\n")
+    with pytest.raises(ios.IOSError):
+        g.load_latency_cache(str(p))
