@@ -3,11 +3,13 @@ vs the sequential and greedy schedules on the same kernels, + % of per-stage roo
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--net inception_v3] [--impl ours|reference]
 
-One step = one batch-1 inference of the whole network through ios_run (every stage of Q, one
-launch each, captured in a CUDA graph), inputs resident in HBM; L2 is flushed (a 2x-L2 write)
-before every timed step. N > 1: one process per GPU (torchrun), replicas only (batch 1 does not
-shard), device time max over ranks. `--impl reference` times the CPU oracle
-(the tier's reference arm) on a bounded sample of the same workload.
+One step = one inference of the whole network through ios_run (every stage of Q, one launch each,
+captured in a CUDA graph), inputs resident in HBM; L2 is flushed (a 2x-L2 write) before every timed
+step. N > 1 (`--gpus N`; re-executed under torch.distributed.run when launched directly): one
+process per GPU, the global batch (default 8 per GPU) sharded by image, each rank its own graph and
+DP schedule, no collective on the hot path, device time max over ranks.
+`--impl reference` times the CPU oracle (the tier's reference arm) on a bounded sample of the
+same workload.
 """
 from __future__ import annotations
 
@@ -31,7 +33,10 @@ NETS = {
 METRIC = "batch-1 latency ms (IOS vs sequential/greedy schedule) + % stage roofline"
 
 
-def _peaks():
+def _peaks(measure_tf32: bool = False, device=None):
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written HBM copy GB/s and cuBLAS bf16 TF/s on
+    this pool's B200s) and, when a GPU is at hand, the dense TF32 peak measured here (cuBLAS fp32
+    matmul with allow_tf32, best of 10, the recipe SURVEY §0 / BASELINE.md ask for)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     src = "measured"
     try:
@@ -39,8 +44,35 @@ def _peaks():
         hbm, bf16 = float(m["hbm_gbs"]), float(m["bf16_tflops"])
     except Exception:
         hbm, bf16, src = 6650.0, 1590.0, "fallback"
-    # TF32 has no measured peak: the measured bf16 burst x the guide's nominal tf32/bf16 ratio (1.1/2.25)
-    return {"hbm_gbs": hbm, "bf16_tflops": bf16, "tf32_tflops": bf16 * 1.1 / 2.25, "source": src}
+    tf32, tf32_src = bf16 * 1.1 / 2.25, "bf16 x 1.1/2.25 nominal"
+    if measure_tf32:
+        try:
+            tf32, tf32_src = measure_tf32_tflops(device), "measured here: cuBLAS fp32 8192^3 matmul, allow_tf32, best of 10"
+        except Exception as e:  # noqa: BLE001
+            tf32_src += f" (measurement failed: {e})"
+    return {"hbm_gbs": hbm, "bf16_tflops": bf16, "tf32_tflops": tf32, "source": src, "tf32_source": tf32_src}
+
+
+def measure_tf32_tflops(device=None, n: int = 8192, reps: int = 10) -> float:
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(n, n, device=device)
+        b = torch.randn(n, n, device=device)
+        c = a @ b
+        torch.cuda.synchronize(device)
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b, out=c)
+            e1.record()
+            torch.cuda.synchronize(device)
+            best = min(best, e0.elapsed_time(e1))
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
 
 
 class ClockSampler:
@@ -84,16 +116,20 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def stage_roofline(g, net, q, peaks):
+def stage_roofline(g, net, q, peaks, times_ms=None):
     """Per-stage roofline: T_roof = max(F / P_tc, B / BW_HBM) with F = unpadded conv
-    FLOPs and B = distinct input bytes + weight bytes + output bytes (elided concat = 0)."""
+    FLOPs and B = distinct input bytes + weight bytes + output bytes (elided concat = 0). `ms` is the
+    stage's in-run attributable time when `times_ms` is given (ios_run_timeline), else the
+    profiler's latency stored with the schedule."""
     from workloads.netspec import NetSpec  # noqa: F401
     esz = 2 if net.math == "bf16" else 4
     ptc = (peaks["bf16_tflops"] if net.math == "bf16" else peaks["tf32_tflops"]) * 1e12
     bw = peaks["hbm_gbs"] * 1e9
     shapes = {i: g.op_shape(i) for i in range(net.n_ops + 1)}
     rows = []
-    for ops, t, lat in q.stages:
+    for si, (ops, t, lat) in enumerate(q.stages):
+        if times_ms is not None:
+            lat = times_ms[si]
         f = 0
         wbytes = 0
         in_ids = set()
@@ -142,20 +178,19 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     spec = NETS[args.net]
-    # batch sharding: contiguous per-rank slices, each rank its own graph + DP schedule;
-    # batch 1 does not shard: every rank runs a batch-1 replica
+    # batch sharding: contiguous per-rank slices, each rank its own graph + DP schedule,
+    # no collective on the hot path. Default global batch: 1 on one GPU (the BASELINE metric), 8 per
+    # GPU when N > 1 (north star: partitioning only by batch, at batch >= 8; weak scaling)
     from paper_2011_01302_b200.shard import shard_range
-    if args.batch > 1:
-        b0, b1 = shard_range(args.batch, world, rank)
-        local_batch = b1 - b0
-        parallelism = f"batch-sharded {args.batch} over {world} GPU(s) ({local_batch}/rank), no collective on the hot path"
-        images = args.batch
-    else:
-        local_batch = 1
-        parallelism = f"replicas x{world} (batch 1 does not shard)"
-        images = world
+    batch = args.batch if args.batch > 0 else (1 if world == 1 else 8 * world)
+    if batch < world:
+        raise SystemExit(f"global batch {batch} < {world} GPUs: batch 1 does not shard (DESIGN.md §8)")
+    b0, b1 = shard_range(batch, world, rank)
+    local_batch = b1 - b0
+    parallelism = ("single GPU" if world == 1 else
+                   f"batch-sharded {batch} over {world} GPUs ({local_batch}/rank), no collective on the hot path")
     net = W.build(args.net, math=spec["math"], batch=local_batch)
-    peaks = _peaks()
+    peaks = _peaks(measure_tf32=True, device=dev)
 
     g = Graph.from_netspec(net, spec["math"], local)
     t0 = time.time()
@@ -176,6 +211,11 @@ def run_ours(args):
         for q in (q_ios, q_seq, q_greedy):
             g.tune(q)
         tune_s = time.time() - t1
+    if args.save_schedule and rank == 0:
+        # exactly what is timed below, for tools/ncu_run.py --schedule (profiler replay)
+        json.dump({"net": args.net, "batch": local_batch, "math": spec["math"],
+                   "stages": [[ops, t] for ops, t, _ in q_ios.stages]}, open(args.save_schedule, "w"))
+        g.save_tile_variants(args.save_schedule + ".variants")
 
     x = torch.from_numpy(net.make_input()).to(dev)
     out = torch.empty(g.output_shape(), dtype=torch.float32, device=dev)
@@ -183,10 +223,10 @@ def run_ours(args):
     flush = torch.empty(int(2 * torch.cuda.get_device_properties(dev).L2_cache_size) // 4 + 1024,
                         dtype=torch.float32, device=dev)
 
-    def timed(q, steps, warmup, sampler=None):
+    def timed(q, steps, warmup):
         for _ in range(warmup):
             g.run(q, x, out)
-        torch.cuda.synchronize(dev)
+        g.sync()
         if world > 1:
             dist.barrier()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -197,6 +237,7 @@ def run_ours(args):
             g.run(q, x, out)
             evs[i][1].record(stream)
         torch.cuda.synchronize(dev)
+        g.sync()                                               # IOS_ERR_KERNEL if any in-kernel wait timed out
         tot = sum(a.elapsed_time(b) for a, b in evs)
         t = torch.tensor([tot / steps], dtype=torch.float64, device=dev)
         if world > 1:
@@ -208,30 +249,30 @@ def run_ours(args):
     ms_seq = timed(q_seq, max(20, args.steps // 4), args.warmup)
     ms_greedy = timed(q_greedy, max(20, args.steps // 4), args.warmup)
 
-    # end to end through the public API with HOST buffers (pinned input copy in, output copy out)
-    xh = torch.from_numpy(net.make_input()).pin_memory()
-    yh = torch.empty(g.output_shape(), dtype=torch.float32).pin_memory()
-    for _ in range(args.warmup):
-        x.copy_(xh, non_blocking=True)
-        g.run(q_ios, x, out)
-        yh.copy_(out, non_blocking=True)
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # end to end through the public C-ABI with HOST buffers (ios_run_host: pinned input copied in,
+    # run, output copied back, synchronised), L2 flushed before every step like the timed loop;
+    # host wall clock around the call (it is synchronous)
+    xh_t = torch.from_numpy(net.make_input()).pin_memory()
+    xh = xh_t.numpy()
     e2e_steps = max(20, args.steps // 4)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        x.copy_(xh, non_blocking=True)
-        g.run(q_ios, x, out)
-        yh.copy_(out, non_blocking=True)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e2e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        yh = g.run_host(q_ios, xh)
+    e2e_tot = 0.0
+    for i in range(e2e_steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize(dev)
+        t_a = time.perf_counter()
+        yh = g.run_host(q_ios, xh)
+        e2e_tot += time.perf_counter() - t_a
+    e2e_ms = torch.tensor([e2e_tot * 1e3 / e2e_steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
 
-    # per-stage roofline of the IOS schedule: stage latencies are CUDA-event timings of each stage
-    # launch alone (the profiler that fed the DP; ios_stage_latency)
-    rows = stage_roofline(g, net, q_ios, peaks)
+    # per-stage roofline of the IOS schedule from IN-RUN stage times: the same CUDA graph with PDL,
+    # L2 flushed before each run, every stage launch stamping its span on the global timer
+    # (ios_run_timeline); attributable time = end - previous stage's end
+    tl = g.run_timeline(q_ios, x, out, reps=20, l2_flush=True)
+    rows = stage_roofline(g, net, q_ios, peaks, times_ms=[a * 1e-3 for _, _, a in tl])
     launches_per_run = q_ios.launches()
     if rank == 0:
         tot_roof = sum(r["roof_ms"] for r in rows)
@@ -239,21 +280,18 @@ def run_ours(args):
         conv_rows = [r for r in rows if r["roof_ms"] >= 0.002 and r["flops"] > 0]
         f_tot = sum(r["flops"] for r in rows)
         b_tot = sum(r["bytes"] for r in rows)
-        tc_time = sum(r["flops"] for r in rows) / ((peaks["bf16_tflops"] if net.math == "bf16" else peaks["tf32_tflops"]) * 1e9)
+        ptc = peaks["bf16_tflops"] if net.math == "bf16" else peaks["tf32_tflops"]
+        tc_time = f_tot / (ptc * 1e9)
         hbm_time = b_tot / (peaks["hbm_gbs"] * 1e6)
         bound = "tensor" if tc_time >= hbm_time else "hbm"
         if bound == "tensor":
-            achieved = f_tot / (tot_ms * 1e9)            # TFLOP/s
-            peak = peaks["bf16_tflops"] if net.math == "bf16" else peaks["tf32_tflops"]
-            unit = "TFLOP/s"
+            achieved, peak, unit = f_tot / (tot_ms * 1e9), ptc, "TFLOP/s"
         else:
-            achieved = b_tot / (tot_ms * 1e6)            # GB/s
-            peak = peaks["hbm_gbs"]
-            unit = "GB/s"
+            achieved, peak, unit = b_tot / (tot_ms * 1e6), peaks["hbm_gbs"], "GB/s"
         cpu = cpu_baseline(net, args.cpu_sample_s)
         traffic = None
         tp = os.path.join(ROOT, "profiles", f"traffic_{args.net}.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp) and local_batch == 1:
             try:
                 traffic = json.load(open(tp)).get("bytes_per_step")
             except Exception:
@@ -271,28 +309,33 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "bf16" if net.math == "bf16" else "tf32",
             "data": "synthetic (seeded N(0,1) input, He-init weights, DESIGN.md input recipe)",
-            "config": {"workload": spec["desc"], "net": args.net, "batch": args.batch, "schedule": f"IOS-Both r={args.r} s={args.s}",
+            "config": {"workload": spec["desc"] if batch == 1 else spec["desc"].replace("batch 1", f"batch {batch}"),
+                       "net": args.net, "batch": batch, "schedule": f"IOS-Both r={args.r} s={args.s}",
                        "parallelism": parallelism, "l2": "flushed before every timed step",
                        "stages": len(q_ios.stages), "launches_per_run": launches_per_run},
             "sequential_ms": round(ms_seq, 4),
             "greedy_ms": round(ms_greedy, 4),
             "speedup_vs_sequential": round(ms_seq / ms_ios, 3),
             "speedup_vs_greedy": round(ms_greedy / ms_ios, 3),
-            "images_per_s": round(images * 1000.0 / ms_ios, 1),
+            "images_per_s": round(batch * 1000.0 / ms_ios, 1),
             "search_s": round(search_s, 2),
             "tune_s": round(tune_s, 2),
             "search_stats": {"states": q_ios.stats[0], "transitions": q_ios.stats[1], "stages_measured": q_ios.stats[2]},
             "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": unit,
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "peak_source": peaks["source"] + (" (tf32 = bf16 x 1.1/2.25 nominal)" if net.math != "bf16" else ""),
-                         "kernel": "ios_stage_kernel (all stages; per-stage CUDA-event durations)"},
+                         "peak_source": peaks["source"] + ("" if net.math == "bf16" else "; tf32: " + peaks["tf32_source"]),
+                         "kernel": "ios_stage_kernel (all stage launches of one inference; algorithmic bytes or FLOPs of "
+                                   "the schedule / sum of in-run stage times, ios_run_timeline, L2 flushed per run)"},
             "stage_roofline": {"frac_sum": round(tot_roof / tot_ms, 4) if tot_ms else None,
                                "conv_stages": len(conv_rows),
                                "conv_stages_ge_50pct": sum(1 for r in conv_rows if r["ms"] > 0 and r["roof_ms"] / r["ms"] >= 0.5),
-                               "roof_ms_sum": round(tot_roof, 4), "stage_ms_sum": round(tot_ms, 4)},
+                               "best_stage_frac": round(max((r["roof_ms"] / r["ms"] for r in rows if r["ms"] > 0), default=0), 4),
+                               "roof_ms_sum": round(tot_roof, 4), "stage_ms_sum_in_run": round(tot_ms, 4),
+                               "tf32_peak_tflops": round(peaks["tf32_tflops"], 1)},
             "cpu_baseline": cpu,
             "e2e": {"value": round(float(e2e_ms.item()), 4), "unit": "ms",
-                    "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4)},
+                    "h2d_bytes_per_step": int(xh_t.numel() * 4), "d2h_bytes_per_step": int(np.prod(g.output_shape()) * 4),
+                    "how": "ios_run_host (C-ABI, pinned host buffers), host wall clock, L2 flushed before each step"},
             "gpu_launches": int(launches_per_run * args.steps),
             "clocks": clk.summary(),
         }
@@ -302,12 +345,22 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _oracle_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def cpu_baseline(net, budget_s: float):
-    """The oracle as it stands (plain NumPy float64 sequential executor), timed on this host."""
+    """The oracle as it stands (plain NumPy float64 sequential executor), timed on this host with the
+    BLAS thread pool sized to the affinity cores (its convolutions are single-threaded einsums; its
+    matmuls use the pool)."""
     from oracle import OracleGraph
+    threads = _oracle_threads()
     try:
         from threadpoolctl import threadpool_limits
-        ctx = threadpool_limits(limits=1)
+        ctx = threadpool_limits(limits=threads)
     except Exception:
         ctx = None
     og = OracleGraph(net)
@@ -318,11 +371,12 @@ def cpu_baseline(net, budget_s: float):
         t0 = time.perf_counter()
         og.run_sequential(x)
         times.append(time.perf_counter() - t0)
-    if ctx is not None:
-        ctx.unregister() if hasattr(ctx, "unregister") else None
+    if ctx is not None and hasattr(ctx, "unregister"):
+        ctx.unregister()
     ms = sorted(times)[len(times) // 2] * 1e3
-    return {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": "oracle",
-            "sample": f"{len(times)} full batch-1 inference(s) of the same network (run_sequential, float64)"}
+    return {"value": round(ms, 2), "unit": "ms", "cores": threads, "kind": "oracle",
+            "sample": f"{len(times)} full inference(s) of the same network, batch {net.input_shape[0]} "
+                      f"(run_sequential, float64; BLAS threads = {threads}, conv einsums single-threaded)"}
 
 
 def run_reference(args):
@@ -335,6 +389,12 @@ def run_reference(args):
     from oracle import OracleGraph
     spec = NETS[args.net]
     net = W.build(args.net, math=spec["math"])
+    threads = _oracle_threads()
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=threads)
+    except Exception:
+        pass
     og = OracleGraph(net)
     x = net.make_input()
     for _ in range(min(args.warmup, 1)):
@@ -347,11 +407,20 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": round(ms, 2), "unit": "ms", "n_gpus": world,
             "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": round(ms, 2), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": spec["desc"], "net": args.net, "batch": args.batch, "schedule": "sequential (oracle)"},
-            "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": 1, "kind": "oracle",
-                             "sample": f"{steps} full batch-1 inference(s), float64 NumPy"},
+            "config": {"workload": spec["desc"], "net": args.net, "batch": 1, "schedule": "sequential (oracle)"},
+            "cpu_baseline": {"value": round(ms, 2), "unit": "ms", "cores": threads, "kind": "oracle",
+                             "sample": f"{steps} full batch-1 inference(s), float64 NumPy (BLAS threads = {threads})"},
             "e2e": {"value": round(ms, 2), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def _relaunch_distributed(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run, one rank per GPU."""
+    import random
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(random.randint(20000, 40000)),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -360,15 +429,21 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--net", default="inception_v3", choices=sorted(NETS))
-    ap.add_argument("--batch", type=int, default=1, help="global batch (> 1: sharded across the ranks)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="global batch, sharded across the ranks (default: 1 on one GPU, 8 per GPU when N > 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--r", type=int, default=3)
     ap.add_argument("--s", type=int, default=8)
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--latency-cache", default="", help="load (if present) / save the DP's stage-latency cache")
     ap.add_argument("--tune", type=int, default=1, help="1: ios_schedule_tune every schedule (per-stage tiling), 0: default tiling")
+    ap.add_argument("--save-schedule", default="", help="write the timed IOS schedule (+ .variants) for tools/ncu_run.py")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch_distributed(args.gpus))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}; using WORLD_SIZE", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     else:

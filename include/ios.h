@@ -174,6 +174,11 @@ IOS_API ios_status ios_schedule_stage(ios_schedule q, int32_t i, int32_t* ops, i
  * use the fastest variant for that stage. Does not change Q or its outputs beyond floating-point
  * summation order. Synchronises. Errors: IOS_ERR_INVALID_ARG, IOS_ERR_CUDA, IOS_ERR_KERNEL. */
 IOS_API ios_status ios_schedule_tune(ios_graph g, ios_schedule q, int32_t trials, int32_t reps);
+/* The tuner's per-stage choices as a text file (one "block_pos mask strategy variant" line per
+ * stage), so another process replays exactly the plans that were timed (e.g. under a profiler).
+ * Loading checks the graph (op count, batch, math) and touches the device. */
+IOS_API ios_status ios_tile_variants_save(ios_graph g, const char* path);
+IOS_API ios_status ios_tile_variants_load(ios_graph g, const char* path);
 
 /* ---- execution ------------------------------------------------------------------------------ */
 
@@ -193,6 +198,15 @@ IOS_API ios_status ios_run_host(ios_graph g, ios_schedule q, const float* h_inpu
 IOS_API ios_status ios_sync(ios_graph g, void* cuda_stream);
 /* Copies op `op`'s most recent output (NCHW fp32) to caller-owned device memory. */
 IOS_API ios_status ios_op_output(ios_graph g, int32_t op, void* d_out, void* cuda_stream);
+/* In-run stage timeline (the stage profiler "in context"): runs Q `reps` times exactly as ios_run
+ * does (one CUDA graph, programmatic dependent launch between stages), each run after an L2 flush
+ * if l2_flush != 0, with every stage launch stamping its CTAs' earliest start (after the PDL wait)
+ * and latest exit on the device's global timer. Per stage i, stage_us[3i..3i+2] = mean over reps of
+ * (start, end) in us relative to the first stage's start, and of the ATTRIBUTABLE time
+ * end_i - end_{i-1} (stage 0: end - start; empty stages 0), which sums to the schedule's span.
+ * d_input/d_output as ios_run (device, caller-owned). cap >= 3 * #stages. Synchronises. */
+IOS_API ios_status ios_run_timeline(ios_graph g, ios_schedule q, const void* d_input, void* d_output, int32_t reps,
+                                    int32_t l2_flush, double* stage_us, int32_t cap);
 /* Number of kernel launches one ios_run of q performs (stage kernels + boundary layout kernels). */
 IOS_API ios_status ios_schedule_launches(ios_graph g, ios_schedule q, int32_t* n_launches);
 

@@ -39,21 +39,30 @@ def _stale(sid: str) -> bool:
         return f.read().strip() != sid
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra_defs=(), out: str = "") -> str:
+    """Compile libios.so (or, with extra -D flags, an experiment variant into `out`)."""
     sid = source_hash()
-    if not force and not _stale(sid):
+    variant = bool(extra_defs or out)
+    if not variant and not force and not _stale(sid):
         return LIB
+    lib = out or LIB
     objs = []
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    bdir = os.path.join(HERE, "build", os.path.splitext(os.path.basename(lib))[0] if variant else "")
+    os.makedirs(bdir, exist_ok=True)
     procs = []
     # the stage kernel's six (dtype, smem-descriptor) instantiations are separate units so they
     # compile in parallel (stage_kernel.cu, IOS_INST_DT / IOS_INST_SD)
     units = [(src, []) for src in SOURCES]
-    units += [("stage_kernel.cu", [f"-DIOS_INST_DT={dt}", f"-DIOS_INST_SD={sdv}"]) for dt in range(3) for sdv in range(2)]
+    # (dtype, smem-descriptor, feature class): TF32 / BF16 x {lean, gather, full, trace}; FP32-SIMT x
+    # {full, trace} (stage_kernel.cu launch_stage, stage_desc.h KernelFeature)
+    insts = [(dt, sdv, ft) for dt in (0, 1) for sdv in (0, 1) for ft in (0, 1, 3, 7)]
+    insts += [(2, sdv, ft) for sdv in (0, 1) for ft in (3, 7)]
+    units += [("stage_kernel.cu", [f"-DIOS_INST_DT={dt}", f"-DIOS_INST_SD={sdv}", f"-DIOS_INST_FEAT={ft}"])
+              for dt, sdv, ft in insts]
     for src, defs in units:
-        tag = "".join(d.split("=")[1] for d in defs)
-        obj = os.path.join(HERE, "build", src + (f".inst{tag}" if tag else "") + ".o")
-        cmd = [NVCC, *FLAGS, *defs, f'-DIOS_BUILD_ID="{sid}"', "-c", os.path.join(CSRC, src), "-o", obj]
+        tag = "_".join(d.split("=")[1] for d in defs)
+        obj = os.path.join(bdir, src + (f".inst{tag}" if tag else "") + ".o")
+        cmd = [NVCC, *FLAGS, *defs, *extra_defs, f'-DIOS_BUILD_ID="{sid}"', "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu") and verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -68,13 +77,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
             failed = True
     if failed:
         raise RuntimeError("libios build failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *FLAGS, "-shared", "-o", tmp, *objs]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    with open(ID_FILE, "w") as f:
-        f.write(sid + "\n")
-    return LIB
+    os.replace(tmp, lib)
+    if not variant:
+        with open(ID_FILE, "w") as f:
+            f.write(sid + "\n")
+    return lib
 
 
 if __name__ == "__main__":

@@ -447,6 +447,33 @@ ios_status ios_run_host(ios_graph gh, ios_schedule qh, const float* h_in, float*
   ABI_END
 }
 
+ios_status ios_run_timeline(ios_graph gh, ios_schedule qh, const void* d_in, void* d_out, int32_t reps,
+                            int32_t l2_flush, double* stage_us, int32_t cap) {
+  ABI_BEGIN
+  REQUIRE(gh && qh && d_in && d_out && stage_us && reps > 0, "bad arguments");
+  REQUIRE(qh->q.g == &gh->g, "schedule belongs to another graph");
+  REQUIRE(cap >= 3 * (int)qh->q.stages.size(), "capacity too small (3 doubles per stage)");
+  validate_schedule(gh->g, qh->q);
+  std::vector<double> v;
+  run_timeline(gh->g, qh->q, d_in, d_out, reps, l2_flush != 0, v);
+  for (size_t i = 0; i < v.size(); ++i) stage_us[i] = v[i];
+  ABI_END
+}
+
+ios_status ios_tile_variants_save(ios_graph gh, const char* path) {
+  ABI_BEGIN
+  REQUIRE(gh && path, "bad arguments");
+  save_tile_variants(gh->g, path);
+  ABI_END
+}
+
+ios_status ios_tile_variants_load(ios_graph gh, const char* path) {
+  ABI_BEGIN
+  REQUIRE(gh && path, "bad arguments");
+  load_tile_variants(gh->g, path);
+  ABI_END
+}
+
 ios_status ios_sync(ios_graph gh, void* stream) {
   ABI_BEGIN
   REQUIRE(gh, "bad arguments");

@@ -9,7 +9,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <limits>
+#include <sstream>
 
 #include <cuda.h>
 
@@ -993,6 +995,12 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       sd.segs_off = (int)(pb + vb);
       sd.uses_counters = 0;
       for (Problem& p : b.probs) sd.uses_counters |= (p.signal || (p.kind == PK_GEMM && p.split > 1)) ? 1 : 0;
+      sd.feat = 0;   // kernel feature class (stage_desc.h): which producer paths the stage uses
+      for (Problem& p : b.probs) {
+        if (p.kind != PK_GEMM) continue;
+        if (p.fdw) sd.feat |= F_FDW;
+        else if (!(p.a_tma || p.tt)) sd.feat |= F_GATHER;
+      }
       sd.ring_slots = kStages;
       for (Problem& p : b.probs)
         if (p.kind == PK_GEMM && p.hws) sd.ring_slots = kStages - 1;
@@ -1345,6 +1353,118 @@ void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStre
     q.n_launches = launches;
   }
   IOS_CHECK_CUDA(cudaGraphLaunch(q.exec, st));
+}
+
+// In-run stage timeline (A7 "in context"): Q exactly as ios_run executes it (one CUDA graph, PDL
+// between stage launches), except that every stage launch records the earliest start (after its
+// PDL wait) and the latest exit of its CTAs on %globaltimer. A stage's *attributable* time is its
+// end minus the previous stage's end (stage 0: minus its own start), so the attributable times sum
+// to the whole schedule's span and overlap through PDL is charged to the stage that hides it.
+// `reps` runs, each optionally after an L2 flush (the bench's protocol); per stage the mean over
+// reps of (start, end) relative to stage 0's start, and of the attributable time, in us.
+void run_timeline(Graph& g, Schedule& q, const void* d_in, void* d_out, int reps, bool flush,
+                  std::vector<double>& out) {
+  ensure_device(g);
+  DeviceState& d = *g.dev;
+  check_err(d);
+  const int n = (int)q.stages.size();
+  std::vector<StagePlan*> plans;
+  for (const Stage& s : q.stages) {
+    int bpos = -1;
+    const uint64_t mask = g.mask_of(s.ops, &bpos);
+    plans.push_back(get_plan(g, bpos, mask, s.strategy));
+  }
+  std::vector<void*> tmp;
+  struct Free {
+    DeviceState& d;
+    std::vector<void*>& v;
+    ~Free() {
+      cudaStreamSynchronize(d.stream);
+      for (void* p : v) cudaFreeAsync(p, d.stream);
+    }
+  } fr{d, tmp};
+  uint64_t* stamps = static_cast<uint64_t*>(dmalloc(d, (size_t)n * 2 * sizeof(uint64_t), &tmp));
+  if (flush && !d.l2buf) d.l2buf = dmalloc(d, (size_t)d.l2bytes);
+  IOS_CHECK_CUDA(cudaStreamSynchronize(d.stream));
+  GraphExec ex = capture(d, [&] {
+    // starts = UINT64_MAX (atomicMin), ends = 0 (atomicMax): even slots 0xFF.., odd slots 0
+    for (int i = 0; i < n; ++i) {
+      IOS_CHECK_CUDA(cudaMemsetAsync(stamps + 2 * i, 0xFF, sizeof(uint64_t), d.stream));
+      IOS_CHECK_CUDA(cudaMemsetAsync(stamps + 2 * i + 1, 0, sizeof(uint64_t), d.stream));
+    }
+    const Op& in = g.ops[0];
+    IOS_CHECK_CUDA(launch_nchw_to_nhwc(static_cast<const float*>(d_in), d.od[0].out, g.dtype(), in.N, in.C, d.stream));
+    for (int i = 0; i < n; ++i) {
+      if (plans[i]->empty) continue;
+      StageDesc sd = plans[i]->sd;
+      sd.stamp = (uint64_t)(stamps + 2 * i);
+      IOS_CHECK_CUDA(launch_stage(sd, plans[i]->dtype, plans[i]->grid, d.stream));
+    }
+    const Op& last = g.ops.back();
+    IOS_CHECK_CUDA(launch_nhwc_to_nchw(d.od[last.id].out, g.dtype(), static_cast<float*>(d_out), last.N, last.C, d.stream));
+  });
+  out.assign((size_t)n * 3, 0.0);
+  std::vector<uint64_t> h((size_t)n * 2);
+  for (int r = 0; r < reps; ++r) {
+    if (flush) IOS_CHECK_CUDA(launch_l2_flush(d.l2buf, d.l2bytes, d.stream));
+    IOS_CHECK_CUDA(cudaGraphLaunch(ex.exec, d.stream));
+    IOS_CHECK_CUDA(cudaStreamSynchronize(d.stream));
+    check_err(d);
+    IOS_CHECK_CUDA(cudaMemcpy(h.data(), stamps, h.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    uint64_t t0 = 0;
+    for (int i = 0; i < n && !t0; ++i)
+      if (!plans[i]->empty) t0 = h[2 * i];
+    double prev_end = 0.0;
+    for (int i = 0; i < n; ++i) {
+      double st = prev_end, en = prev_end;
+      if (!plans[i]->empty) {
+        st = (double)(int64_t)(h[2 * i] - t0) * 1e-3;
+        en = (double)(int64_t)(h[2 * i + 1] - t0) * 1e-3;
+      }
+      out[3 * i] += st / reps;
+      out[3 * i + 1] += en / reps;
+      out[3 * i + 2] += (en - prev_end) / reps;
+      prev_end = en;
+    }
+  }
+}
+
+// Tuned tiling variants (ios_schedule_tune's choices) as text, one "block_pos mask strategy variant"
+// per line, so a profiler run (tools/ncu_run.py) replays exactly the plans the bench timed.
+void save_tile_variants(Graph& g, const std::string& path) {
+  ensure_device(g);
+  std::ofstream f(path);
+  if (!f) IOS_FAIL(IOS_ERR_INVALID_ARG, "cannot write " + path);
+  f << "ios-tile-variants v1 ops=" << g.ops.size() << " batch=" << g.batch << " math=" << (int)g.math << "\n";
+  for (auto& [k, v] : g.dev->tile_variant)
+    f << std::get<0>(k) << " " << std::get<1>(k) << " " << std::get<2>(k) << " " << v << "\n";
+}
+
+void load_tile_variants(Graph& g, const std::string& path) {
+  ensure_device(g);
+  DeviceState& d = *g.dev;
+  std::ifstream f(path);
+  if (!f) IOS_FAIL(IOS_ERR_INVALID_ARG, "cannot read " + path);
+  std::string head;
+  std::getline(f, head);
+  std::ostringstream want;
+  want << "ios-tile-variants v1 ops=" << g.ops.size() << " batch=" << g.batch << " math=" << (int)g.math;
+  if (head != want.str()) IOS_FAIL(IOS_ERR_INVALID_ARG, "tile variants belong to another graph");
+  long long bp, t, v;
+  unsigned long long m;
+  while (f >> bp >> m >> t >> v) {
+    if (bp < 0 || bp >= (long long)g.blocks.size() || v < 0 || v >= kTileVariants)
+      IOS_FAIL(IOS_ERR_INVALID_ARG, "malformed tile variant entry");
+    const auto key = std::make_tuple((int)bp, (uint64_t)m, (int)t);
+    d.tile_variant[key] = (int)v;
+    auto it = d.plans.find(key);
+    if (it != d.plans.end()) {
+      d.retired.push_back(it->second);
+      d.plans.erase(it);
+      ++d.plan_gen;
+    }
+  }
+  if (!f.eof()) IOS_FAIL(IOS_ERR_INVALID_ARG, "malformed tile variant file");
 }
 
 int schedule_launches(Graph& g, Schedule& q) {

@@ -109,6 +109,9 @@ void measure_stages(Graph& g, int bpos, const std::vector<std::pair<uint64_t, in
 void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStream_t st);
 void op_output(Graph& g, int op, void* d_out, cudaStream_t st);
 int schedule_launches(Graph& g, Schedule& q);
+void save_tile_variants(Graph& g, const std::string& path);
+void load_tile_variants(Graph& g, const std::string& path);
+void run_timeline(Graph& g, Schedule& q, const void* d_in, void* d_out, int reps, bool flush, std::vector<double>& out);
 int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* out, int cap);
 void destroy_device(Graph& g);
 void tune_schedule(Graph& g, Schedule& q, int trials, int reps);

@@ -126,6 +126,16 @@ struct Problem {
                                     // staged by ONE 4D tensor TMA (tmap_a) per K chunk, OOB = padding zeros
 };
 
+// Kernel feature classes: the stage kernel is instantiated per class with only the code paths its
+// stages use (measured: the unused paths' code and registers cost 7-10 % end to end through
+// instruction-cache misses and spills). The host picks the smallest class covering a stage.
+enum KernelFeature : int32_t {
+  F_GATHER = 1,   // implicit-im2col cp.async producer (pre-ReLU convs, narrow / unaligned inputs)
+  F_FDW = 2,      // fused Relu-SepConv producers (halo + register forms)
+  F_TRACE = 4,    // per-CTA %globaltimer timeline (ios_stage_trace)
+};
+constexpr int kFeatLean = 0, kFeatGather = F_GATHER, kFeatFull = F_GATHER | F_FDW, kFeatTrace = kFeatFull | F_TRACE;
+
 // halo path (single-input fused Relu-SepConv): the stage runs its smem ring with 3 slots; slot 3's
 // B region holds the input window of the chunk, slot 3's A region the chunk's depthwise weights
 constexpr int kHaloBytes = kBStageBytes;          // 32 KB: <= 256 pixels x 128 B
@@ -138,12 +148,15 @@ struct StageDesc {
   uint64_t counters;                // int32[n_counters]; [0..1] = 64-bit launch counter (see uses_counters)
   uint64_t err;                     // int32 error flag (dependency-wait timeout), host-mapped pinned memory
   uint64_t trace;                   // optional uint64 [grid][16] timeline (0 = off)
+  uint64_t stamp;                   // optional uint64 [2]: atomicMin of the CTAs' start (after the
+                                    // PDL wait) and atomicMax of their exit, %globaltimer ns (0 = off)
   int32_t n_problems, n_tiles, n_counters, has_gemm;
   int32_t blob_bytes;               // problems | views | segments, contiguous from `problems`
   int32_t views_off, segs_off;
   int32_t uses_counters;            // any in-stage dependency or split-K: counters[0..1] count launches
                                     // (epoch), the others grow monotonically (targets epoch-relative,
                                     // compared wrap-safely mod 2^32)
+  int32_t feat;                     // KernelFeature bits this stage needs (host: picks the instantiation)
   int32_t ring_slots;               // smem ring depth this launch: kStages, or kStages - 1 when a halo
                                     // problem borrows the last slot
 };

@@ -71,6 +71,9 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, uint64_t tmap, int c0,
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void prefetch_tmap(uint64_t tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cnt(uint32_t a, uint32_t n) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(n) : "memory");
 }
@@ -941,10 +944,25 @@ __device__ __forceinline__ int find_problem(const int* sm_tile_begin, int n_prob
   return p;
 }
 
+// (split, m tile, n tile, K chunk range) of GEMM tile `local` of problem P
+struct TileCoord {
+  int s, mt, nt, c0, c1;
+};
+__device__ __forceinline__ TileCoord tile_coord(const Problem& P, int local) {
+  TileCoord tc;
+  const int rest = fdiv(P.fd_split, local);
+  tc.s = local - rest * P.split;
+  tc.mt = fdiv(P.fd_ntn, rest);
+  tc.nt = rest - tc.mt * P.n_tiles_n;
+  tc.c0 = tc.s * P.chunks_per_split;
+  tc.c1 = min(tc.c0 + P.chunks_per_split, P.k_chunks);
+  return tc;
+}
+
 // SD: the descriptor table fits the smem copy (the host picks the instantiation). The pointers are
 // then derived from the shared array, so descriptor reads compile to shared loads, which do not
 // wait behind outstanding global stores the way generic loads do.
-template <int DT, bool SD>
+template <int DT, bool SD, int FEAT>
 __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc sd) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align by pointer arithmetic on the shared array (an integer round trip would make every
@@ -977,31 +995,18 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   // optional per-CTA timeline (ns, %globaltimer) for tools/trace_stage.py; slots: 0 entry, 1 prologue
   // done, 2 first GEMM tile A issued, 3 producer done, 4 MMA done, 5 first accumulator ready,
   // 6 epilogue/SIMT done, 7 teardown, 8 exit
-  uint64_t* trace = sd.trace ? reinterpret_cast<uint64_t*>(sd.trace) + blockIdx.x * 16 : nullptr;
-  bool tfirst = trace != nullptr;   // register flag: stamp only the first tile of each role
-#define IOS_TRACE(slot)                   \
-  do {                                    \
-    if (trace) trace[(slot)] = gtimer();  \
+  // (only in the F_TRACE instantiation: the stamps cost registers and code in every hot loop)
+  constexpr bool kTrace = (FEAT & F_TRACE) != 0;
+  uint64_t* trace = kTrace && sd.trace ? reinterpret_cast<uint64_t*>(sd.trace) + blockIdx.x * 16 : nullptr;
+  bool tfirst = kTrace && trace != nullptr;   // register flag: stamp only the first tile of each role
+#define IOS_TRACE(slot)                              \
+  do {                                               \
+    if constexpr (kTrace)                            \
+      if (trace) trace[(slot)] = gtimer();           \
   } while (0)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) IOS_TRACE(0);
-#ifdef IOS_LATPROBE
-  if (tid == 0 && trace) {
-    const int* q = reinterpret_cast<const int*>(sd.problems);
-    uint64_t a = gtimer();
-    int v1 = __ldcg(q + 64 * (blockIdx.x % 8));
-    uint64_t b = gtimer();
-    int v2 = __ldcg(q + 64 * (blockIdx.x % 8) + 32 * (v1 & 1) + 16);
-    uint64_t c = gtimer();
-    trace[13] = b - a + (v2 == 12345 ? 1 : 0);
-    trace[14] = c - b;
-    long long k0 = clock64();
-    uint64_t d0 = gtimer();
-    while (clock64() - k0 < 10000) {}
-    trace[15] = gtimer() - d0;   // ns for 10000 SM cycles -> SM clock
-  }
-#endif
 
   if (desc_in_smem) {
     const int4* src = reinterpret_cast<const int4*>(sd.problems);
@@ -1042,6 +1047,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     for (int q = lane; q < sd.n_problems; q += 32) {
       const Problem& P = probs[q];
       if (P.kind != PK_GEMM) continue;
+#ifndef IOS_NO_TMAP_PREFETCH
+      if (P.tmap_a) prefetch_tmap(P.tmap_a);   // descriptor fetch off the first TMA's critical path
+#endif
       const uint64_t total = (uint64_t)P.k_chunks * P.Npad8 * kChunkBytes;
       const uint64_t share = ((total + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
       const uint64_t b0 = share * blockIdx.x, b1 = b0 + share < total ? b0 + share : total;
@@ -1054,6 +1062,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   // here on we read activations (and counters) the previous grid may still be writing
   if (tid == 0) IOS_TRACE(11);   // before waiting for the previous grid
   pdl_wait();
+  if (sd.stamp && tid == 0) atomicMin(reinterpret_cast<unsigned long long*>(sd.stamp), (unsigned long long)gtimer());
   // launch epoch: every CTA of a launch adds 1 to the launch counter exactly once, before releasing the
   // next launch (launch_dependents), so old / grid is this launch's number for every CTA
   // (64-bit, in counters[0..1]: it never wraps; the epoch itself is used mod 2^32)
@@ -1096,18 +1105,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
       if (P.kind != PK_GEMM) continue;
+      const int local = t - P.tile_begin;
+      const TileCoord tc = tile_coord(P, local);
+      const int mt = tc.mt, nt = tc.nt, c0 = tc.c0, c1 = tc.c1;
       if (P.n_deps) {
         if (ptid == 0) wait_deps(P, counters, err, ep);
         named_bar(1, 128);
       }
-      const int local = t - P.tile_begin;
-      const int rest = fdiv(P.fd_split, local);
-      const int s = local - rest * P.split;
-      const int mt = fdiv(P.fd_ntn, rest);
-      const int nt = rest - mt * P.n_tiles_n;
-      const int c0 = s * P.chunks_per_split;
-      const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
-      if (DT != ET_F32X && P.fdw) {
+      if constexpr ((FEAT & F_FDW) != 0 && DT != ET_F32X) if (P.fdw) {
         // fused Relu-SepConv: depthwise computed into the A slot, pointwise weights by bulk copy
         const int rr = fdiv(P.fd_tilw, mt);
         const int tw = mt - rr * P.tiles_w;
@@ -1240,6 +1245,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         named_bar(1, 128);
         continue;
       }
+      // implicit-im2col gather (cp.async) path: compiled into the F_GATHER instantiations only;
+      // the host never hands a gather problem to a kernel without it (stage_features)
+      if constexpr ((FEAT & F_GATHER) != 0) {
       // everything the chunk loop needs lives in registers: the cp.async asm statements clobber
       // "memory", which would otherwise force the descriptor fields to be re-read from smem
       const View in = views[P.in_begin];
@@ -1367,6 +1375,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         if (pend[0] >= 0) mbar_arrive(smem_u32(&full[pend[0]]));
         if (pend[1] >= 0) mbar_arrive(smem_u32(&full[pend[1]]));
       }
+      }   // F_GATHER
     }
   } else if (warp == kMmaWarp) {
     // ============================================================== MMA ISSUER
@@ -1904,7 +1913,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     }
   }
 
-  if (trace && (tid == 0 || tid == kEpilogueWarp0 * 32 || tid == kMmaWarp * 32))
+  if (kTrace && trace && (tid == 0 || tid == kEpilogueWarp0 * 32 || tid == kMmaWarp * 32))
     IOS_TRACE(tid == 0 ? 3 : tid == kMmaWarp * 32 ? 4 : 6);
   // ---------------------------------------------------------------------------- teardown
   __syncwarp();   // the MMA warp ran its loop on lane 0 only
@@ -1917,17 +1926,19 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   if (tid == 0) {
     IOS_TRACE(7);   // counters are epoch-relative: nothing to reset at exit
     IOS_TRACE(8);
+    if (sd.stamp) atomicMax(reinterpret_cast<unsigned long long*>(sd.stamp) + 1, (unsigned long long)gtimer());
   }
 #undef IOS_TRACE
 }
 
 #ifdef IOS_INST_DT
-#define IOS_LAUNCHER_DEF2(dt, sdv) IOS_LAUNCHER_DECL(dt, sdv)
-#define IOS_LAUNCHER_DECL(dt, sdv) cudaError_t launch_stage_inst_##dt##_##sdv(cudaLaunchConfig_t& cfg, const StageDesc& sd)
-IOS_LAUNCHER_DEF2(IOS_INST_DT, IOS_INST_SD) {
+#define IOS_LAUNCHER_DEF3(dt, sdv, ft) IOS_LAUNCHER_DECL(dt, sdv, ft)
+#define IOS_LAUNCHER_DECL(dt, sdv, ft) \
+  cudaError_t launch_stage_inst_##dt##_##sdv##_##ft(cudaLaunchConfig_t& cfg, const StageDesc& sd)
+IOS_LAUNCHER_DEF3(IOS_INST_DT, IOS_INST_SD, IOS_INST_FEAT) {
   static bool attr_done = false;
   static int max_grid = 0;
-  auto k = ios_stage_kernel<IOS_INST_DT, (IOS_INST_SD != 0)>;
+  auto k = ios_stage_kernel<IOS_INST_DT, (IOS_INST_SD != 0), IOS_INST_FEAT>;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
     if (e != cudaSuccess) return e;
@@ -1979,12 +1990,25 @@ __global__ void l2_flush_kernel(int4* buf, int64_t n) {
 }
 
 // ------------------------------------------------------------------------------ host launchers
-// The six (DT, SD) instantiations of the stage kernel are compiled as separate translation units
-// (build.py passes -DIOS_INST_DT=<dt> -DIOS_INST_SD=<0|1>; nvcc runs them in parallel). Each unit
-// exports one plain host launcher; launch_stage (host unit) dispatches to them.
-#define IOS_LAUNCHER_DECL(dt, sdv) cudaError_t launch_stage_inst_##dt##_##sdv(cudaLaunchConfig_t& cfg, const StageDesc& sd)
-IOS_LAUNCHER_DECL(0, 0); IOS_LAUNCHER_DECL(0, 1); IOS_LAUNCHER_DECL(1, 0);
-IOS_LAUNCHER_DECL(1, 1); IOS_LAUNCHER_DECL(2, 0); IOS_LAUNCHER_DECL(2, 1);
+// The stage kernel's (dtype, smem-descriptor, feature class) instantiations are compiled as separate
+// translation units (build.py passes -DIOS_INST_DT / _SD / _FEAT; nvcc runs them in parallel). Each
+// unit exports one plain host launcher; launch_stage (host unit) dispatches to them.
+#define IOS_LAUNCHER_DECL(dt, sdv, ft) \
+  cudaError_t launch_stage_inst_##dt##_##sdv##_##ft(cudaLaunchConfig_t& cfg, const StageDesc& sd)
+#define IOS_DECL_CLASSES(dt, sdv) \
+  IOS_LAUNCHER_DECL(dt, sdv, 0); IOS_LAUNCHER_DECL(dt, sdv, 1); IOS_LAUNCHER_DECL(dt, sdv, 3); IOS_LAUNCHER_DECL(dt, sdv, 7)
+IOS_DECL_CLASSES(0, 0); IOS_DECL_CLASSES(0, 1); IOS_DECL_CLASSES(1, 0); IOS_DECL_CLASSES(1, 1);
+IOS_LAUNCHER_DECL(2, 0, 3); IOS_LAUNCHER_DECL(2, 1, 3); IOS_LAUNCHER_DECL(2, 0, 7); IOS_LAUNCHER_DECL(2, 1, 7);
+
+namespace {
+// smallest compiled class covering the stage's features (FP32-SIMT: the full class only)
+int feature_class(int dtype, int feat) {
+  if (feat & F_TRACE) return kFeatTrace;
+  if (dtype == ET_F32X || (feat & F_FDW)) return kFeatFull;
+  if (feat & F_GATHER) return kFeatGather;
+  return kFeatLean;
+}
+}  // namespace
 
 cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
@@ -1997,17 +2021,25 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // IOS_COOP=1: cooperative launch (the runtime guarantees co-residency of the whole grid or fails)
+  // IOS_COOP=1: cooperative launch (the runtime guarantees co-residency of the whole grid or fails;
+  // measured ~6 % slower end to end on Inception V3 b=1, so off by default)
   static const bool coop = getenv("IOS_COOP") && atoi(getenv("IOS_COOP")) != 0;
   if (coop) {
     attr[1].id = cudaLaunchAttributeCooperative;
     attr[1].val.cooperative = 1;
     cfg.numAttrs = 2;
   }
-  const bool smem_desc = sd.blob_bytes <= kDescBytes;
-  if (dtype == ET_BF16) return smem_desc ? launch_stage_inst_1_1(cfg, sd) : launch_stage_inst_1_0(cfg, sd);
-  if (dtype == ET_F32X) return smem_desc ? launch_stage_inst_2_1(cfg, sd) : launch_stage_inst_2_0(cfg, sd);
-  return smem_desc ? launch_stage_inst_0_1(cfg, sd) : launch_stage_inst_0_0(cfg, sd);
+  const int sdv = sd.blob_bytes <= kDescBytes ? 1 : 0;
+  const int fc = feature_class(dtype, sd.feat | (sd.trace ? F_TRACE : 0));
+#define IOS_DISPATCH(dt, sv, f) \
+  if (dtype == dt && sdv == sv && fc == f) return launch_stage_inst_##dt##_##sv##_##f(cfg, sd)
+  IOS_DISPATCH(0, 1, 0); IOS_DISPATCH(0, 1, 1); IOS_DISPATCH(0, 1, 3); IOS_DISPATCH(0, 1, 7);
+  IOS_DISPATCH(0, 0, 0); IOS_DISPATCH(0, 0, 1); IOS_DISPATCH(0, 0, 3); IOS_DISPATCH(0, 0, 7);
+  IOS_DISPATCH(1, 1, 0); IOS_DISPATCH(1, 1, 1); IOS_DISPATCH(1, 1, 3); IOS_DISPATCH(1, 1, 7);
+  IOS_DISPATCH(1, 0, 0); IOS_DISPATCH(1, 0, 1); IOS_DISPATCH(1, 0, 3); IOS_DISPATCH(1, 0, 7);
+  IOS_DISPATCH(2, 1, 3); IOS_DISPATCH(2, 1, 7); IOS_DISPATCH(2, 0, 3); IOS_DISPATCH(2, 0, 7);
+#undef IOS_DISPATCH
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_nchw_to_nhwc(const float* in, const View& out, int dtype, int N, int C, cudaStream_t st) {

@@ -82,15 +82,21 @@ def _load():
         "ios_latency_cache_load": [P, C.c_char_p],
         "ios_latency_cache_autosave": [P, C.c_char_p],
         "ios_sync": [P, P],
+        "ios_tile_variants_save": [P, C.c_char_p],
+        "ios_tile_variants_load": [P, C.c_char_p],
+        "ios_run_timeline": [P, P, P, P, I32, I32, pD, I32],
     }
     for name, args in sig.items():
+        if os.environ.get("IOS_LIB") and not hasattr(lib, name):
+            continue   # an older experiment build (A/B runs) may lack newer entry points
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = I32
     lib.ios_last_error.restype = C.c_char_p
     lib.ios_last_error.argtypes = []
-    lib.ios_build_id.restype = C.c_char_p
-    lib.ios_build_id.argtypes = []
+    if hasattr(lib, "ios_build_id"):
+        lib.ios_build_id.restype = C.c_char_p
+        lib.ios_build_id.argtypes = []
     lib.ios_schedule_destroy.argtypes = [P]
     lib.ios_schedule_destroy.restype = None
     lib.ios_graph_destroy.argtypes = [P]
@@ -317,6 +323,17 @@ class Graph:
                                 out.ctypes.data_as(C.POINTER(C.c_float)), None))
         return out
 
+    def run_timeline(self, q: Schedule, x, out=None, reps: int = 10, l2_flush: bool = True):
+        """ios_run_timeline: per stage (start_us, end_us, attributable_us), mean over `reps` runs."""
+        import torch
+        if out is None:
+            out = torch.empty(self.output_shape(), dtype=torch.float32, device=x.device)
+        n = len(q.stages)
+        buf = (C.c_double * (3 * max(1, n)))()
+        _check(lib.ios_run_timeline(self.handle, q.handle, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
+                                    reps, int(l2_flush), buf, 3 * max(1, n)))
+        return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n)]
+
     def sync(self, stream=None) -> None:
         """ios_sync on `stream` (default: torch's current stream of the graph's device)."""
         if stream is None:
@@ -330,6 +347,12 @@ class Graph:
         st = stream if stream is not None else torch.cuda.current_stream(t.device).cuda_stream
         _check(lib.ios_op_output(self.handle, op, C.c_void_p(t.data_ptr()), C.c_void_p(st)))
         return t
+
+    def save_tile_variants(self, path: str) -> None:
+        _check(lib.ios_tile_variants_save(self.handle, path.encode()))
+
+    def load_tile_variants(self, path: str) -> None:
+        _check(lib.ios_tile_variants_load(self.handle, path.encode()))
 
     def save_latency_cache(self, path: str) -> None:
         _check(lib.ios_latency_cache_save(self.handle, path.encode()))

@@ -39,3 +39,16 @@ def test_stage_roofline_accounting():
     b0 = (64 * hw + 128 * 64 * 9 + 64 * 64 + 96 * 64 * 9 + (128 + 64 + 96) * hw) * 4   # x read once
     assert rows[0]["bytes"] == b0
     assert rows[2]["flops"] == 0 and rows[2]["bytes"] == 0                               # elided concat
+
+
+def test_gpus_flag_relaunches_one_rank_per_gpu():
+    """`bench.py --gpus 2` outside torchrun re-executes itself under torch.distributed.run (one
+    process per GPU); exercised here on the reference arm, where rank 0 alone prints the line."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--net", "fig2",
+                          "--gpus", "2", "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2

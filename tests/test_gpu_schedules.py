@@ -1,0 +1,188 @@
+"""GPU parity for the schedules the product actually runs (VERDICT r1 "what's missing" 2):
+DP-chosen schedules (device-searched, and fixed cost tables that force chains, multi-group stages
+and merges) on every BASELINE network, FP32-SIMT at 1e-5 on a full network, batch > 1, the host-buffer
+entry point, batch sharding, and the stage profiler's sanity checks.
+
+Every check compares the CUDA path (through the C-ABI) with the oracle on the same seeded inputs:
+per op (the oracle fed the GPU's own inputs, Z13) and end to end.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import OracleGraph
+from tests.gpu_util import TOL, per_op_errors, rel_err
+
+pytestmark = pytest.mark.gpu
+
+NETS = [("inception_v3", "tf32"), ("squeezenet", "tf32"), ("randwire_ws_small", "bf16"), ("nasnet_a_large", "tf32")]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return torch
+
+
+def _popcount(m):
+    return bin(m).count("1")
+
+
+def _check_run(net, math, g, q, torch, ops=None):
+    """Run q, then per-op parity (every op, or `ops`) and end-to-end parity."""
+    x = net.make_input()
+    y = g.run(q, torch.from_numpy(x).cuda())
+    g.sync()
+    errs = per_op_errors(net, g, math, ops=ops)
+    worst = max(errs, key=errs.get)
+    assert errs[worst] < TOL.get(math, 1e-5), (worst, net.op(worst).name, errs[worst])
+    ref = OracleGraph(net).run_sequential(x)[net.n_ops]
+    assert rel_err(y.cpu().numpy(), ref) < TOL.get(math, 1e-5)
+    return errs
+
+
+def _has_chain_stage(net, q):
+    for ops, _, _ in q.stages:
+        s = set(ops)
+        if any(u in s for v in ops for u in net.op(v).inputs):
+            return True
+    return False
+
+
+@pytest.mark.parametrize("name,math", NETS)
+def test_fewest_stages_schedule_chains_and_groups(torch_cuda, name, math):
+    """A fixed cost table (every stage costs the same) makes the DP pick the fewest stages under
+    P(3, 8): stages with intra-group chains (in-kernel counters) and several groups. Per op + end to end."""
+    from paper_2011_01302_b200 import Graph
+    net = W.build(name, math=math)
+    g = Graph.from_netspec(net, math)
+    q = g.schedule_dp(3, 8, lambda b, m, t: 1.0 + (0.5 if t == 1 else 0.0))
+    assert _has_chain_stage(net, q)
+    assert max(len(ops) for ops, _, _ in q.stages) >= 3
+    _check_run(net, math, g, q, torch_cuda)
+
+
+@pytest.mark.parametrize("name,math", [("inception_v3", "tf32"), ("squeezenet", "tf32")])
+def test_forced_merge_schedule(torch_cuda, name, math):
+    """IOS-Merge with a cost table that makes every legal merge win: the DP merges all it can.
+    Inception: the Mixed_5b 1x1 triple, Mixed_7b's 1x1 triple and its 1x3 + 3x1 pairs (bounding box
+    3x3); SqueezeNet: every fire expand pair. Per op + end to end."""
+    from paper_2011_01302_b200 import Graph, MERGE
+    net = W.build(name, math=math)
+    g = Graph.from_netspec(net, math)
+    q = g.schedule_dp(3, 8, lambda b, m, t: 1.0 if t == MERGE else float(_popcount(m)), strategies="merge")
+    merged = [sorted(ops) for ops, t, _ in q.stages if t == MERGE]
+    if name == "inception_v3":
+        for want in ([8, 9, 11], [97, 98, 101], [99, 100], [103, 104]):
+            assert want in merged, (want, merged)
+    else:
+        assert [4, 5] in merged and [8, 9] in merged
+    _check_run(net, math, g, q, torch_cuda)
+
+
+@pytest.mark.parametrize("name,math,r,s", [("inception_v3", "tf32", 3, 8), ("squeezenet", "tf32", 3, 8),
+                                           ("randwire_ws_small", "bf16", 2, 3), ("nasnet_a_large", "tf32", 1, 3)])
+def test_device_searched_and_tuned_ios_schedule(torch_cuda, name, math, r, s):
+    """The schedule bench.py times: the DP over device-measured stage latencies, then stage-tuned.
+    (RandWire / NASNet use tighter pruning here only to keep the search within the test budget.)"""
+    from paper_2011_01302_b200 import Graph
+    net = W.build(name, math=math)
+    g = Graph.from_netspec(net, math)
+    q = g.schedule_dp(r, s)
+    g.tune(q)
+    _check_run(net, math, g, q, torch_cuda)
+
+
+def test_inception_fp32_simt_per_op_1e5(torch_cuda):
+    """IOS_MATH_FP32_SIMT (exact fp32 storage, CUDA-core FMA GEMM) on the whole of Inception V3:
+    the north star's 1e-5, per op and end to end, under the greedy schedule (multi-group stages)."""
+    from paper_2011_01302_b200 import Graph
+    net = W.build("inception_v3")
+    g = Graph.from_netspec(net, "fp32_simt")
+    errs = _check_run(net, "fp32_simt", g, g.schedule_greedy(), torch_cuda)
+    assert max(errs.values()) < 1e-5
+
+
+@pytest.mark.parametrize("name,batch", [("squeezenet", 8), ("inception_v3", 8)])
+def test_batch8_network(torch_cuda, name, batch):
+    """Batch 8 (the multi-GPU shard size): sequential and device-searched IOS schedules."""
+    from paper_2011_01302_b200 import Graph
+    net = W.build(name, batch=batch)
+    g = Graph.from_netspec(net, "tf32")
+    _check_run(net, "tf32", g, g.schedule_sequential(), torch_cuda)
+    _check_run(net, "tf32", g, g.schedule_dp(3, 8), torch_cuda, ops=[])
+
+
+def test_run_host_matches_run(torch_cuda):
+    """ios_run_host (host buffers in and out, the e2e path) == ios_run bit for bit, and == oracle."""
+    from paper_2011_01302_b200 import Graph
+    net = W.build("inception_v3")
+    g = Graph.from_netspec(net, "tf32")
+    q = g.schedule_dp(3, 8)
+    x = net.make_input()
+    y_dev = g.run(q, torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+    y_host = g.run_host(q, x)
+    # not bitwise: split-K partials are reduced with fp32 atomics in arrival order (
+    # IOS_SLAB_SPLITS gives a bitwise-reproducible mode), and TF32 storage rounding can amplify a
+    # last-bit difference to 2^-11 relative
+    assert rel_err(y_host, y_dev) < 1e-3
+    ref = OracleGraph(net).run_sequential(x)[net.n_ops]
+    assert rel_err(y_host, ref) < TOL["tf32"]
+
+
+def test_fake_shard_equals_unsharded(torch_cuda):
+    """Batch sharding without a second GPU: the 4 shards of a batch-8 SqueezeNet run
+    one after another on this device (each its own graph at batch 2 and its own DP schedule, as the
+    ranks would) and their concatenated outputs match the unsharded batch-8 run and the oracle."""
+    from paper_2011_01302_b200 import Graph
+    from paper_2011_01302_b200.shard import shard_range
+    full = W.build("squeezenet", batch=8)
+    x = full.make_input()
+    g = Graph.from_netspec(full, "tf32")
+    y_full = g.run(g.schedule_dp(3, 8), torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+    parts = []
+    for rank in range(4):
+        b0, b1 = shard_range(8, 4, rank)
+        net = W.build("squeezenet", batch=b1 - b0)
+        gs = Graph.from_netspec(net, "tf32")
+        parts.append(gs.run(gs.schedule_dp(3, 8), torch_cuda.from_numpy(np.ascontiguousarray(x[b0:b1])).cuda()).cpu().numpy())
+    y_sh = np.concatenate(parts, axis=0)
+    assert rel_err(y_sh, y_full) < TOL["tf32"]
+    ref = OracleGraph(full).run_sequential(x)[full.n_ops]
+    assert rel_err(y_sh, ref) < TOL["tf32"]
+
+
+def test_stage_profiler_sanity(torch_cuda):
+    """SURVEY §8c A7 sanity checks of ios_stage_latency (a measurement: parity unpinned):
+    (1) profiled stage latencies agree with the same stages' in-run times (ios_run_timeline: the
+    schedule's CUDA graph with PDL, per-stage spans on the global timer) — in sum within 15 %, and
+    per stage within a factor 2.5; (2) no stage runs faster than its roofline;
+    (3) run-to-run spread of the profiler below 10 % (after a first, clock-ramping measurement)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import _peaks, stage_roofline
+    from paper_2011_01302_b200 import Graph
+    torch = torch_cuda
+    net = W.build("inception_v3")
+    g = Graph.from_netspec(net, "tf32")
+    x = torch.from_numpy(net.make_input()).cuda()
+    q = g.schedule_dp(3, 8)
+    out = g.run(q, x)
+    g.sync()
+    tl = g.run_timeline(q, x, out, reps=10, l2_flush=True)
+    prof = [g.stage_latency(ops, t) * 1e3 for ops, t, _ in q.stages]
+    inrun = [a for _, _, a in tl]
+    assert abs(sum(inrun) - sum(prof)) / sum(prof) < 0.15, (sum(inrun), sum(prof))          # (1)
+    for p, a, (ops, _, _) in zip(prof, inrun, q.stages):
+        if p > 2.0:                                                                          # non-empty stages
+            assert 1 / 2.5 < a / p < 2.5, (ops, p, a)
+    rows = stage_roofline(g, net, q, _peaks(), times_ms=[a * 1e-3 for a in inrun])
+    for r in rows:
+        if r["ms"] > 0:
+            assert r["ms"] >= r["roof_ms"], r                                                 # (2)
+    for op in (5, 42, 99):                 # big-M 1x1, 17x17 1x7, 8x8 1x3 (swap-AB)
+        t = [g.stage_latency([op], 0, trials=5, reps=20) for _ in range(5)][1:]
+        med = float(np.median(t))
+        assert (max(t) - min(t)) / med < 0.10, (op, t)                                       # (3)
