@@ -210,9 +210,10 @@ IOS_API ios_status ios_run_timeline(ios_graph g, ios_schedule q, const void* d_i
 /* Number of kernel launches one ios_run of q performs (stage kernels + boundary layout kernels). */
 IOS_API ios_status ios_schedule_launches(ios_graph g, ios_schedule q, int32_t* n_launches);
 
-/* Diagnostic timeline of ONE launch of a stage: per CTA 16 uint64 %globaltimer stamps (ns; 0 = not
- * reached): 0 entry, 1 prologue done, 2 first A chunk issued, 3 producer done, 4 MMA done,
- * 5 first accumulator ready, 6 epilogue/SIMT done, 7 teardown, 8 exit. out must hold grid*16. */
+/* Diagnostic timeline of ONE launch of a stage: per CTA 16 uint64 stamps (0 = not reached): slot 0
+ * = %globaltimer ns at the CTA's entry, slots 1-15 = SM clock cycles since that entry, plus 1:
+ * 1 prologue done, 2 first A chunk issued, 3 producer done, 4 MMA done, 5 first accumulator ready,
+ * 6 epilogue/SIMT done, 7 teardown, 8 exit, 9-15 path-specific. out must hold grid*16. */
 IOS_API ios_status ios_stage_trace(ios_graph g, const int32_t* ops, int32_t n_ops, ios_strategy t, uint64_t* out,
                                    int32_t cap, int32_t* grid);
 

@@ -7,6 +7,7 @@
 //   runner      (A9): the stages of Q in order, captured once into a CUDA graph
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -844,10 +845,32 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       p.n_tiles = (p.n_items + p.items_per_tile - 1) / p.items_per_tile;
       simt_tiles += p.n_tiles;
     }
-    std::vector<GemmSpec*> gs;
-    for (size_t i = 0; i < b.probs.size(); ++i)
-      if (b.probs[i].kind == PK_GEMM) gs.push_back(&b.specs[i]);
-    choose_tiling(gs, simt_tiles, d.num_sms, variant);
+    // Phase-aware tiling: members of one intra-group chain never run at the same time (a member
+    // waits for its producer's completion counter), so each dependency phase (0 = no in-stage
+    // producer, k = 1 + the latest producer's phase) is sized to fill the SMs on its own, instead of
+    // all members sharing one wave (measured on Inception Mixed_5b: the 5x5 and 3x3 links of the
+    // chains got 20-40 CTAs with 14-27 K chunks each).
+    // (opt-in, IOS_PHASE_TILING=1: measured 2 % slower on the Inception V3 IOS schedule -- the extra
+    // split-K reductions of the first links cost more than the shorter K loops of the later ones)
+    static const bool phased = getenv("IOS_PHASE_TILING") && atoi(getenv("IOS_PHASE_TILING")) != 0;
+    std::vector<int> phase(b.probs.size(), 0);
+    int n_phases = 1;
+    for (size_t i = 0; i < b.probs.size(); ++i) {
+      for (int k = 0; k < b.probs[i].n_deps; ++k)   // dep_idx still holds problem indices here
+        phase[i] = std::max(phase[i], phase[b.probs[i].dep_idx[k]] + 1);
+      n_phases = std::max(n_phases, phase[i] + 1);
+    }
+    if (!phased) std::fill(phase.begin(), phase.end(), 0), n_phases = 1;
+    for (int ph = 0; ph < n_phases; ++ph) {
+      std::vector<GemmSpec*> gs;
+      int ph_simt = 0;
+      for (size_t i = 0; i < b.probs.size(); ++i) {
+        if (phase[i] != ph) continue;
+        if (b.probs[i].kind == PK_GEMM) gs.push_back(&b.specs[i]);
+        else ph_simt += b.probs[i].n_tiles;
+      }
+      if (!gs.empty()) choose_tiling(gs, phased ? ph_simt : simt_tiles, d.num_sms, variant);
+    }
     size_t ws_bytes = 0;
     int n_tilectr = 0;
     for (size_t i = 0; i < b.probs.size(); ++i) {
@@ -1001,13 +1024,43 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
         if (p.fdw) sd.feat |= F_FDW;
         else if (!(p.a_tma || p.tt)) sd.feat |= F_GATHER;
       }
-      sd.ring_slots = kStages;
-      for (Problem& p : b.probs)
-        if (p.kind == PK_GEMM && p.hws) sd.ring_slots = kStages - 1;
+      // ring: slots sized for the stage's widest B operand (weights BN x 128 B, or the swap-AB pixel
+      // operand), as many as fit kRingBytes: a 128 x 32 tile ring is 9 deep instead of 4. A stage
+      // with a halo-path fused sepconv keeps the fixed 3 x 48 KB ring (the 4th slot holds its windows).
+      int max_bn = 16;
+      bool halo = false;
+      for (Problem& p : b.probs) {
+        if (p.kind != PK_GEMM) continue;
+        // (a swap-AB plain-TMA tile's pixel box is always 128 rows, whatever its BN)
+        max_bn = std::max(max_bn, (p.swap_ab && p.a_tma) ? kBM : p.BN);
+        halo |= p.hws != 0;
+      }
+      static const int deep = getenv("IOS_DEEP_RING") ? atoi(getenv("IOS_DEEP_RING")) : 1;
+      if (halo || !deep) {
+        sd.slot_bytes = kAStageBytes + kBStageBytes;
+        sd.ring_slots = halo ? kStages - 1 : kStages;
+      } else {
+        sd.slot_bytes = kAStageBytes + round_up(max_bn * kChunkBytes, 1024);
+        sd.ring_slots = std::min(kMaxSlots, kRingBytes / sd.slot_bytes);
+      }
       sd.has_gemm = 0;
       for (Problem& p : b.probs) sd.has_gemm |= p.kind == PK_GEMM;
       plan->grid = std::min(tiles, d.num_sms);
       plan->dtype = g.dtype();
+      static const bool dump = getenv("IOS_DUMP_PLANS") && atoi(getenv("IOS_DUMP_PLANS")) != 0;
+      if (dump) {   // diagnostics: one line per problem of every plan built
+        fprintf(stderr, "[plan] block %d mask %llx T %d variant %d: %d tiles, grid %d, %d slots x %d B, feat %d\n", bpos,
+                (unsigned long long)mask, strategy, variant, tiles, plan->grid, sd.ring_slots, sd.slot_bytes, sd.feat);
+        for (size_t i = 0; i < b.probs.size(); ++i) {
+          const Problem& p = b.probs[i];
+          if (p.kind == PK_GEMM)
+            fprintf(stderr, "[plan]   gemm M %d N %d K %d kch %d | BN %d ntn %d mt %d split %d cps %d | swap %d tma %d tt %d fdw %d deps %d\n",
+                    p.M, b.specs[i].N16, p.K, p.k_chunks, p.BN, p.n_tiles_n, p.m_tiles, p.split, p.chunks_per_split,
+                    p.swap_ab, p.a_tma, p.tt, p.fdw, p.n_deps);
+          else
+            fprintf(stderr, "[plan]   simt kind %d tiles %d items %d deps %d\n", p.kind, p.n_tiles, p.n_items, p.n_deps);
+        }
+      }
     }
   } catch (...) {
     free_plan(d, plan);
@@ -1299,6 +1352,10 @@ int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* o
   uint64_t* buf = static_cast<uint64_t*>(dmalloc(d, n * sizeof(uint64_t)));
   StageDesc sd = p->sd;
   sd.trace = (uint64_t)buf;
+  // the traced (F_TRACE) instantiation runs once untimed first: its code is then in the SMs'
+  // instruction caches like the production kernel's is in back-to-back runs (IOS_TRACE_COLD=1 skips)
+  static const bool cold = getenv("IOS_TRACE_COLD") && atoi(getenv("IOS_TRACE_COLD")) != 0;
+  if (!cold) IOS_CHECK_CUDA(launch_stage(sd, p->dtype, p->grid, d.stream));
   IOS_CHECK_CUDA(launch_stage(sd, p->dtype, p->grid, d.stream));
   IOS_CHECK_CUDA(cudaStreamSynchronize(d.stream));
   std::vector<uint64_t> h(n);

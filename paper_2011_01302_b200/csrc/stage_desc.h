@@ -10,15 +10,17 @@ namespace ios {
 // ---- tile geometry -----------------------------------------------------------------------------
 constexpr int kBM = 128;                  // GEMM tile rows (output pixels); UMMA M = 128, cta_group::1
 constexpr int kChunkBytes = 128;          // bytes of K per pipeline stage (32 fp32 / 64 bf16 elements)
-constexpr int kStages = 4;                // smem ring depth
+constexpr int kStages = 4;                // ring depth at the widest tile (BN = 256): 4 x 48 KB
 constexpr int kMaxBN = 256;               // UMMA N <= 256
 constexpr int kAStageBytes = kBM * kChunkBytes;         // 16 KB
 constexpr int kBStageBytes = kMaxBN * kChunkBytes;      // 32 KB
-constexpr int kBarBytes = 256;            // mbarriers, TMEM slot, flags
+constexpr int kRingBytes = kStages * (kAStageBytes + kBStageBytes);   // 192 KB of ring slots
+constexpr int kMaxSlots = 16;             // deepest ring (narrow tiles: slot = 16 KB A + BN x 128 B)
+constexpr int kBarBytes = 512;            // mbarriers, TMEM slot, flags
 constexpr int kBiasBytes = 2 * kMaxBN * 4; // bias slice per accumulator buffer
 constexpr int kDescBytes = 14 * 1024;     // stage descriptor table (problems | views | segments) copy
 constexpr int kEpiBytes = 4 * 4096;       // epilogue staging: 32 rows x 128 B per epilogue warp
-constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + kBarBytes + kBiasBytes + kDescBytes + kEpiBytes;
+constexpr int kSmemBytes = kRingBytes + kBarBytes + kBiasBytes + kDescBytes + kEpiBytes;
 constexpr int kProducerWarps = 4;         // warps 0-3: A gather (cp.async) + B bulk copy
 constexpr int kEpilogueWarp0 = 4;         // warps 4-7: TMEM -> registers -> global; SIMT tiles
 constexpr int kMmaWarp = 8;               // warp 8: tcgen05.mma issuer + TMEM allocator
@@ -157,7 +159,10 @@ struct StageDesc {
                                     // (epoch), the others grow monotonically (targets epoch-relative,
                                     // compared wrap-safely mod 2^32)
   int32_t feat;                     // KernelFeature bits this stage needs (host: picks the instantiation)
-  int32_t ring_slots;               // smem ring depth this launch: kStages, or kStages - 1 when a halo
+  int32_t slot_bytes;               // ring slot stride: A region (16 KB: 128 rows x 128 B) then the B region
+                                    // (the stage's widest B operand, BN rows x 128 B, rounded to 1 KB);
+                                    // narrow tiles get a deeper ring (more bytes in flight per CTA)
+  int32_t ring_slots;               // smem ring depth this launch (<= kMaxSlots), or 3 x 48 KB when a halo
                                     // problem borrows the last slot
 };
 

@@ -968,16 +968,18 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   // align by pointer arithmetic on the shared array (an integer round trip would make every
   // derived pointer generic: generic loads wait behind outstanding global stores)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sA = smem;                                       // kStages x 16 KB
-  uint8_t* sB = smem + kStages * kAStageBytes;              // kStages x 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStageBytes);
-  uint64_t* full = bars;                                    // [kStages]
-  uint64_t* empty = bars + kStages;                         // [kStages]
-  uint64_t* tfull = bars + 2 * kStages;                     // [2]
-  uint64_t* tempty = bars + 2 * kStages + 2;                // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  // ring slot s: A region (16 KB) at smem + s * slot_bytes, B region right after it
+  const int slot_bytes = sd.slot_bytes;
+  auto slotA = [&](int s) { return smem + s * slot_bytes; };
+  auto slotB = [&](int s) { return smem + s * slot_bytes + kAStageBytes; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+  uint64_t* full = bars;                                    // [kMaxSlots]
+  uint64_t* empty = bars + kMaxSlots;                       // [kMaxSlots]
+  uint64_t* tfull = bars + 2 * kMaxSlots;                   // [2]
+  uint64_t* tempty = bars + 2 * kMaxSlots + 2;              // [2]
+  uint64_t* hbar = bars + 2 * kMaxSlots + 4;                // [2] halo + depthwise weights landed (halo path)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxSlots + 6);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
-  uint64_t* hbar = bars + 16;                               // [2] halo + depthwise weights landed (halo path)
   float* sbias_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // 2 x kMaxBN
   uint8_t* sdesc = reinterpret_cast<uint8_t*>(bars) + kBarBytes + kBiasBytes;           // kDescBytes
   uint8_t* sepi = sdesc + kDescBytes;                                                     // kEpiBytes: 4 x 4 KB
@@ -999,10 +1001,13 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   constexpr bool kTrace = (FEAT & F_TRACE) != 0;
   uint64_t* trace = kTrace && sd.trace ? reinterpret_cast<uint64_t*>(sd.trace) + blockIdx.x * 16 : nullptr;
   bool tfirst = kTrace && trace != nullptr;   // register flag: stamp only the first tile of each role
-#define IOS_TRACE(slot)                              \
-  do {                                               \
-    if constexpr (kTrace)                            \
-      if (trace) trace[(slot)] = gtimer();           \
+  // slot 0 = %globaltimer ns at entry (aligns CTAs); the other slots = SM cycles since entry + 1
+  // (clock64 is a cheap register read; %globaltimer reads cost ~1 us each and distorted the timeline)
+  const long long t_entry = kTrace ? clock64() : 0;
+#define IOS_TRACE(slot)                                                        \
+  do {                                                                         \
+    if constexpr (kTrace)                                                      \
+      if (trace) trace[(slot)] = (slot) == 0 ? gtimer() : (uint64_t)(clock64() - t_entry + 1); \
   } while (0)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -1016,7 +1021,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   for (int i = tid; i < sd.n_problems; i += kThreads)
     sm_tile_begin[i] = reinterpret_cast<const Problem*>(sd.problems)[i].tile_begin;
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < sd.ring_slots; ++s) {
       mbar_init(smem_u32(&full[s]), kProducerWarps + 1);   // 4 producer warps + the expect_tx arrival
       mbar_init(smem_u32(&empty[s]), 1);
     }
@@ -1106,6 +1111,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const Problem& P = probs[hint];
       if (P.kind != PK_GEMM) continue;
       const int local = t - P.tile_begin;
+      if (ptid == 0 && tfirst) IOS_TRACE(3);
       const TileCoord tc = tile_coord(P, local);
       const int mt = tc.mt, nt = tc.nt, c0 = tc.c0, c1 = tc.c1;
       if (P.n_deps) {
@@ -1126,8 +1132,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           // zeros) and one bulk copy the chunk's depthwise weights; the items are then computed
           // from shared memory. Double-buffered: chunk c+1's window is in flight while chunk c is
           // computed (slot 3's B region = 2 windows of 16 KB, its A region = 2 x 8 KB of weights).
-          const uint32_t hbuf0 = smem_u32(sB + (kStages - 1) * kBStageBytes);
-          const uint32_t wbuf0 = smem_u32(sA + (kStages - 1) * kAStageBytes);
+          // (halo stages run 3 slots of 48 KB; the 4th slot's regions hold the windows / weights)
+          const uint32_t hbuf0 = smem_u32(slotB(kStages - 1));
+          const uint32_t wbuf0 = smem_u32(slotA(kStages - 1));
           const uint32_t hbytes = (uint32_t)(P.hws * P.hhs) * kChunkBytes;
           const uint32_t wbytes = (uint32_t)(P.dk * P.dk * kChunkBytes / ESZ) * 4u;
           const int ih0 = toh0 * P.ds - P.dp, iw0 = tow0 * P.ds - P.dp;
@@ -1147,13 +1154,13 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             if (ptid == 0) {
               const uint32_t fb = smem_u32(&full[ring.slot]);
               mbar_arrive_expect_tx(fb, bbytes);
-              bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
+              bulk_g2s(smem_u32(slotB(ring.slot)), wsrc + c * wstep, bbytes, fb);
               if (c + 1 < c1) issue(c + 1, b ^ 1);
             }
             mbar_wait(smem_u32(&hbar[b]), (hphase >> b) & 1u);
             hphase ^= 1u << b;
             fdw_halo_dispatch<DT>(P, hbuf0 + b * (kHaloBytes / 2), wbuf0 + b * (kHaloWBytes / 2),
-                                  smem_u32(sA + ring.slot * kAStageBytes), toh0, ptid);
+                                  smem_u32(slotA(ring.slot)), toh0, ptid);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&full[ring.slot]));
@@ -1168,9 +1175,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           if (ptid == 0) {
             const uint32_t fb = smem_u32(&full[ring.slot]);
             mbar_arrive_expect_tx(fb, bbytes);
-            bulk_g2s(smem_u32(sB + ring.slot * kBStageBytes), wsrc + c * wstep, bbytes, fb);
+            bulk_g2s(smem_u32(slotB(ring.slot)), wsrc + c * wstep, bbytes, fb);
           }
-          fdw_dispatch<DT>(P, views, smem_u32(sA + ring.slot * kAStageBytes), c, tn0, toh0, tow0, ptid);
+          fdw_dispatch<DT>(P, views, smem_u32(slotA(ring.slot)), c, tn0, toh0, tow0, ptid);
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&full[ring.slot]));   // one arrival per producer warp
@@ -1195,9 +1202,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)(wrow0 >> 3) * 1024;
           const int64_t wstep = (int64_t)(P.Npad8 >> 3) * 1024;
           const uint32_t bbytes = (uint32_t)min(wrows, P.Npad8 - wrow0) * kChunkBytes;
-          uint8_t* const wbuf = swap ? sA : sB;
-          uint8_t* const xbuf = swap ? sB : sA;
-          const int wsb = swap ? kAStageBytes : kBStageBytes, xsb = swap ? kBStageBytes : kAStageBytes;
+          const int woff = swap ? 0 : kAStageBytes, xoff = swap ? kAStageBytes : 0;   // region in a slot
           const int xrow0 = swap ? 0 : mt * kBM;
           // tap-TMA patch origin (input coordinates of tap (0, 0)) and box bytes
           int tn0 = 0, ih0 = 0, iw0 = 0;
@@ -1218,23 +1223,24 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             if (lane == 0) {
               const uint32_t fb = smem_u32(&full[ring.slot]);
               mbar_arrive_expect_tx(fb, xbytes + bbytes);
+              if (tfirst && c == c0) IOS_TRACE(9);
               if (P.tt) {
                 const int tap = fdiv(P.fd_kblk, c);
                 const int cb = c - tap * kblk;
                 const int ti = fdiv(P.fd_kw, tap);
                 const int tj = tap - ti * kwid;
-                tma_load_4d(smem_u32(xbuf + ring.slot * xsb), tmap, cb * ELEMS, iw0 + tj, ih0 + ti, tn0, fb);
+                tma_load_4d(smem_u32(slotA(ring.slot) + xoff), tmap, cb * ELEMS, iw0 + tj, ih0 + ti, tn0, fb);
               } else {
-                tma_load_2d(smem_u32(xbuf + ring.slot * xsb), tmap, c * ELEMS, xrow0, fb);
+                tma_load_2d(smem_u32(slotA(ring.slot) + xoff), tmap, c * ELEMS, xrow0, fb);
               }
-              bulk_g2s(smem_u32(wbuf + ring.slot * wsb), wsrc + c * wstep, bbytes, fb);
+              if (tfirst && c == c0) IOS_TRACE(10);
+              bulk_g2s(smem_u32(slotA(ring.slot) + woff), wsrc + c * wstep, bbytes, fb);
               mbar_arrive_cnt(fb, kProducerWarps);   // stands in for the 4 producer warps' arrivals
-              if (tfirst && c - c0 < 3) IOS_TRACE(c == c0 ? 2 : 8 + c - c0);
+              if (tfirst && c - c0 < 2) IOS_TRACE(c == c0 ? 2 : 12);
             }
             __syncwarp();
             ring.next();
           }
-          if (lane == 0 && tfirst) IOS_TRACE(12);
           tfirst = false;
         } else {
           ring.advance(c1 - c0);
@@ -1284,14 +1290,12 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(P.wts) + (int64_t)(wrow0 >> 3) * 1024;
       const int64_t wstep = (int64_t)(P.Npad8 >> 3) * 1024;
       const uint32_t bbytes = (uint32_t)min(wrows, P.Npad8 - wrow0) * kChunkBytes;
-      uint8_t* const wbuf = swap ? sA : sB;
-      uint8_t* const xbuf = swap ? sB : sA;
-      const int wsb = swap ? kAStageBytes : kBStageBytes, xsb = swap ? kBStageBytes : kAStageBytes;
+      const int woff = swap ? 0 : kAStageBytes, xoff = swap ? kAStageBytes : 0;   // region in a slot
       const char* ibase = reinterpret_cast<const char*>(in.ptr) + (int64_t)in.coff * ESZ;
       // pre-ReLU convs: the gather stays asynchronous; once a chunk's copies have landed, each thread
       // applies the ReLU in place to the 8 pieces it copied itself (visible to it after wait_group)
       auto relu_pieces = [&](int slot) {
-        const uint32_t b0 = smem_u32(xbuf + slot * xsb) + rig * 16 + pc0 * 128;
+        const uint32_t b0 = smem_u32(slotA(slot) + xoff) + rig * 16 + pc0 * 128;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (roff[j] == INT_MIN) continue;
@@ -1321,9 +1325,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         if (ptid == 0) {
           const uint32_t fb = smem_u32(&full[ring.slot]);
           mbar_arrive_expect_tx(fb, bbytes);
-          bulk_g2s(smem_u32(wbuf + ring.slot * wsb), wsrc + c * wstep, bbytes, fb);
+          bulk_g2s(smem_u32(slotA(ring.slot) + woff), wsrc + c * wstep, bbytes, fb);
         }
-        const uint32_t a_st = smem_u32(xbuf + ring.slot * xsb) + rig * 16 + pc0 * 128;
+        const uint32_t a_st = smem_u32(slotA(ring.slot) + xoff) + rig * 16 + pc0 * 128;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const bool kvalid = ti[h] < kh;                            // k < K
@@ -1406,8 +1410,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         for (int c = c0; c < c1; ++c) {
           mbar_wait(smem_u32(&full[ring.slot]), ring.phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + ring.slot * kAStageBytes);
-          const uint32_t b0 = smem_u32(sB + ring.slot * kBStageBytes);
+          const uint32_t a0 = smem_u32(slotA(ring.slot));
+          const uint32_t b0 = smem_u32(slotB(ring.slot));
           __syncwarp();
           if (elect_one()) {
 #pragma unroll
@@ -1652,8 +1656,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const int bn = BNx;
         for (int c = c0; c < c1; ++c) {
           mbar_wait(smem_u32(&full[ering.slot]), ering.phase);
-          const uint8_t* As = sA + ering.slot * kAStageBytes + (etid >> 3) * 1024 + (etid & 7) * 16;
-          const uint8_t* Bs = sB + ering.slot * kBStageBytes;
+          const uint8_t* As = slotA(ering.slot) + (etid >> 3) * 1024 + (etid & 7) * 16;
+          const uint8_t* Bs = slotB(ering.slot);
           float a[32];
 #pragma unroll
           for (int pc = 0; pc < 8; ++pc) {
@@ -1913,8 +1917,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     }
   }
 
-  if (kTrace && trace && (tid == 0 || tid == kEpilogueWarp0 * 32 || tid == kMmaWarp * 32))
-    IOS_TRACE(tid == 0 ? 3 : tid == kMmaWarp * 32 ? 4 : 6);
+  if (kTrace && trace && (tid == kEpilogueWarp0 * 32 || tid == kMmaWarp * 32))
+    IOS_TRACE(tid == kMmaWarp * 32 ? 4 : 6);
   // ---------------------------------------------------------------------------- teardown
   __syncwarp();   // the MMA warp ran its loop on lane 0 only
   tc_fence_before();

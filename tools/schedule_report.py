@@ -48,7 +48,9 @@ if a.trace:
         _check(lib.ios_stage_trace(g.handle, _i32(ops), len(ops), t, buf, 148 * 16, C.byref(grid)))
         arr = np.array(buf[:grid.value * 16], dtype=np.int64).reshape(grid.value, 16)
         t0 = arr[:, 0][arr[:, 0] > 0].min()
-        rel = np.where(arr > 0, (arr - t0) / 1000.0, np.nan)
+        ent = (arr[:, :1] - t0) / 1000.0      # slot 0 globaltimer ns; others SM cycles + 1 (ios.h)
+        rel = np.where(arr > 0, ent + (arr - 1) / 1965.0, np.nan)
+        rel[:, 0] = ent[:, 0]
         print(f"stage {ops} T={t} {r['ms']*1e3:.1f} us (roof {r['roof_ms']*1e3:.2f}), grid {grid.value}; "
               "us since first entry (min/median/max over CTAs):")
         for k, nm in enumerate(names):

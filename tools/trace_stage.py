@@ -15,10 +15,15 @@ for ops, t in stages:
     grid = C.c_int32()
     _check(lib.ios_stage_trace(g.handle, _i32(ops), len(ops), t, buf, 148 * 16, C.byref(grid)))
     a = np.array(buf[:grid.value * 16], dtype=np.int64).reshape(grid.value, 16)[:, :16]
+    # slot 0: globaltimer ns at CTA entry; slots 1-15: SM cycles since entry + 1 (ios.h)
+    ghz = float(os.environ.get("IOS_SM_GHZ", "1.965"))
     t0 = a[:, 0][a[:, 0] > 0].min()
-    rel = np.where(a > 0, (a - t0) / 1000.0, np.nan)
+    ent = (a[:, :1] - t0) / 1000.0
+    rel = np.where(a > 0, ent + (a - 1) / (ghz * 1000.0), np.nan)
+    rel[:, 0] = ent[:, 0]
     print(f"stage {ops} T={t} profiled {ms*1e3:.1f} us, grid {grid.value}; us since first entry (min/median/max over CTAs):")
-    names = ["entry", "prologue", "A1 issued", "prod done", "mma done", "acc1 ready", "epi done", "teardown", "exit", "A2 issued", "A3 issued", "own prologue", "A landed", "e:reds issued", "e:rendezvous", "e:stored1"]
+    names = ["entry", "prologue", "P 1st issued", "P tile start", "mma done", "acc1 ready", "epi done", "teardown", "exit",
+             "P expect_tx", "P A issued", "own prologue", "P 2nd issued", "e:13", "e:14", "e:15"]
     for k, nm in enumerate(names):
         col = rel[:, k]
         col = col[~np.isnan(col)]
