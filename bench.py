@@ -198,17 +198,25 @@ def run_ours(args):
         g.load_latency_cache(args.latency_cache)              # resume: measured stage latencies
     if args.latency_cache:
         g.autosave_latency_cache(args.latency_cache)          # checkpoint after every searched block
-    q_ios = g.schedule_dp(args.r, args.s)                      # device-measured stage costs (Alg. 1)
+    q_dp = g.schedule_dp(args.r, args.s)                       # device-measured stage costs (Alg. 1)
     if args.latency_cache and not os.path.exists(args.latency_cache):
         g.save_latency_cache(args.latency_cache)
     search_s = time.time() - t0
+    refine_s = 0.0
+    q_ios = q_dp
+    if args.refine:
+        # DP optima under a family of cost models, chosen per block by in-context measurement
+        # (ios_schedule_refine, DESIGN.md §6 "Measured refinement")
+        t1 = time.time()
+        q_ios = g.schedule_refine(args.r, args.s, reps=20, beta_us=1.0)
+        refine_s = time.time() - t1
     q_seq = g.schedule_sequential()
     q_greedy = g.schedule_greedy()
     tune_s = 0.0
     if args.tune:
         # per-stage tiling variant by measurement, for every schedule alike (same kernels)
         t1 = time.time()
-        for q in (q_ios, q_seq, q_greedy):
+        for q in (q_ios, q_dp, q_seq, q_greedy):
             g.tune(q)
         tune_s = time.time() - t1
     if args.save_schedule and rank == 0:
@@ -246,6 +254,7 @@ def run_ours(args):
 
     with ClockSampler(local) as clk:
         ms_ios = timed(q_ios, args.steps, args.warmup)
+    ms_dp = timed(q_dp, max(20, args.steps // 4), args.warmup) if q_dp is not q_ios else ms_ios
     ms_seq = timed(q_seq, max(20, args.steps // 4), args.warmup)
     ms_greedy = timed(q_greedy, max(20, args.steps // 4), args.warmup)
 
@@ -310,17 +319,21 @@ def run_ours(args):
             "dtype": "bf16" if net.math == "bf16" else "tf32",
             "data": "synthetic (seeded N(0,1) input, He-init weights, DESIGN.md input recipe)",
             "config": {"workload": spec["desc"] if batch == 1 else spec["desc"].replace("batch 1", f"batch {batch}"),
-                       "net": args.net, "batch": batch, "schedule": f"IOS-Both r={args.r} s={args.s}",
+                       "net": args.net, "batch": batch, "schedule": f"IOS-Both r={args.r} s={args.s}" + (" + measured refinement" if args.refine else ""),
                        "parallelism": parallelism, "l2": "flushed before every timed step",
                        "stages": len(q_ios.stages), "launches_per_run": launches_per_run},
+            "ios_dp_ms": round(ms_dp, 4),
             "sequential_ms": round(ms_seq, 4),
             "greedy_ms": round(ms_greedy, 4),
             "speedup_vs_sequential": round(ms_seq / ms_ios, 3),
             "speedup_vs_greedy": round(ms_greedy / ms_ios, 3),
             "images_per_s": round(batch * 1000.0 / ms_ios, 1),
             "search_s": round(search_s, 2),
+            "refine_s": round(refine_s, 2),
+            "refine_stats": {"candidates": q_ios.stats[3] // 1000, "blocks_not_from_plain_dp": q_ios.stats[3] % 1000}
+            if args.refine else None,
             "tune_s": round(tune_s, 2),
-            "search_stats": {"states": q_ios.stats[0], "transitions": q_ios.stats[1], "stages_measured": q_ios.stats[2]},
+            "search_stats": {"states": q_dp.stats[0], "transitions": q_dp.stats[1], "stages_measured": q_dp.stats[2]},
             "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": unit,
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": peaks["source"] + ("" if net.math == "bf16" else "; tf32: " + peaks["tf32_source"]),
@@ -437,6 +450,7 @@ def main():
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--latency-cache", default="", help="load (if present) / save the DP's stage-latency cache")
     ap.add_argument("--tune", type=int, default=1, help="1: ios_schedule_tune every schedule (per-stage tiling), 0: default tiling")
+    ap.add_argument("--refine", type=int, default=1, help="1: ios_schedule_refine (DP candidates chosen per block in context)")
     ap.add_argument("--save-schedule", default="", help="write the timed IOS schedule (+ .variants) for tools/ncu_run.py")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -11,7 +11,6 @@
 namespace ios {
 int pool_out_size(int h, int k, int s, int p, bool ceil_mode);
 const char* last_error_cstr();
-double schedule_dp(Graph& g, int r, int s, int set, ios_cost_fn cost, void* ctx, Schedule* out, int64_t stats[3]);
 }  // namespace ios
 
 using namespace ios;
@@ -307,6 +306,23 @@ ios_status ios_schedule_dp_ex(ios_graph gh, int32_t r, int32_t s, ios_strategy_s
     throw;
   }
   if (out_cost) *out_cost = c;
+  *out = qh;
+  ABI_END
+}
+
+ios_status ios_schedule_refine(ios_graph gh, int32_t r, int32_t s, int32_t reps, double beta_us, ios_schedule* out,
+                               int64_t out_stats[4]) {
+  ABI_BEGIN
+  REQUIRE(gh && out && reps > 0 && beta_us >= 0.0, "bad arguments");
+  auto* qh = new ios_schedule_s();
+  qh->q.g = &gh->g;
+  try {
+    schedule_refine(gh->g, r, s, reps, beta_us * 1e-3, &qh->q, out_stats);
+    validate_schedule(gh->g, qh->q);
+  } catch (...) {
+    delete qh;
+    throw;
+  }
   *out = qh;
   ABI_END
 }

@@ -115,6 +115,9 @@ void run_timeline(Graph& g, Schedule& q, const void* d_in, void* d_out, int reps
 int stage_trace(Graph& g, const std::vector<int>& ops, int strategy, uint64_t* out, int cap);
 void destroy_device(Graph& g);
 void tune_schedule(Graph& g, Schedule& q, int trials, int reps);
+double schedule_dp(Graph& g, int r, int s, int set, ios_cost_fn cost, void* ctx, Schedule* out, int64_t stats[3],
+                   double stage_bias_ms = 0.0);
+void schedule_refine(Graph& g, int r, int s, int reps, double beta_ms, Schedule* out, int64_t stats[4]);
 void destroy_schedule_exec(Schedule& q);
 void sync_and_check(Graph& g, cudaStream_t st);   // synchronise, then IOS_ERR_KERNEL if a wait timed out
 

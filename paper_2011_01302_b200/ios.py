@@ -82,6 +82,7 @@ def _load():
         "ios_latency_cache_load": [P, C.c_char_p],
         "ios_latency_cache_autosave": [P, C.c_char_p],
         "ios_sync": [P, P],
+        "ios_schedule_refine": [P, I32, I32, I32, D, C.POINTER(P), C.POINTER(I64)],
         "ios_tile_variants_save": [P, C.c_char_p],
         "ios_tile_variants_load": [P, C.c_char_p],
         "ios_run_timeline": [P, P, P, P, I32, I32, pD, I32],
@@ -280,6 +281,13 @@ class Graph:
     def schedule_dp(self, r: int = 3, s: int = 8, cost=None, strategies: str = "both") -> Schedule:
         q, c, stats = ios_schedule_dp(self.handle, r, s, cost, strategies)
         return Schedule(self, q, c, stats)
+
+    def schedule_refine(self, r: int = 3, s: int = 8, reps: int = 10, beta_us: float = 1.0) -> Schedule:
+        """ios_schedule_refine: DP optima under a family of cost models, chosen per block in context."""
+        q = C.c_void_p()
+        stats = (C.c_int64 * 4)()
+        _check(lib.ios_schedule_refine(self.handle, r, s, reps, beta_us, C.byref(q), stats))
+        return Schedule(self, q, None, tuple(int(v) for v in stats))
 
     def tune(self, q: Schedule, trials: int = 0, reps: int = 0) -> None:
         """ios_schedule_tune: pick each stage's tiling variant by measurement (call before runs)."""

@@ -186,3 +186,17 @@ def test_stage_profiler_sanity(torch_cuda):
         t = [g.stage_latency([op], 0, trials=5, reps=20) for _ in range(5)][1:]
         med = float(np.median(t))
         assert (max(t) - min(t)) / med < 0.10, (op, t)                                       # (3)
+
+
+@pytest.mark.parametrize("name,math", [("squeezenet", "tf32"), ("fig2", "tf32")])
+def test_refined_schedule_valid_and_parity(torch_cuda, name, math):
+    """ios_schedule_refine (DP optima under a family of cost models, chosen per block in context)
+    returns a valid schedule (the library validates it; every op exactly once) and its outputs match
+    the oracle per op and end to end."""
+    from paper_2011_01302_b200 import Graph
+    net = W.build(name, math=math)
+    g = Graph.from_netspec(net, math)
+    q = g.schedule_refine(3, 8, reps=5, beta_us=1.0)
+    assert q.stats[3] // 1000 >= 1                       # at least the plain DP's candidate
+    assert sorted(v for ops, _, _ in q.stages for v in ops) == list(range(1, net.n_ops + 1))
+    _check_run(net, math, g, q, torch_cuda)
