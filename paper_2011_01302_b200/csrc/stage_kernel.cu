@@ -96,7 +96,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) {
-  __syncwarp();   // bar.sync is .aligned: reconverge lanes that diverged (e.g. one lane spun on a counter)
+  // bar.sync is .aligned: every warp arrives converged (the dependency / split-K spins that precede
+  // these barriers are run by whole warps with warp-uniform exit conditions; synccheck-clean)
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ int fdiv(const FastDiv& f, int x) {
@@ -303,35 +305,35 @@ __device__ __forceinline__ bool before(int c, uint32_t target) { return (int)((u
 __device__ __forceinline__ void flag_error(int* err) {
   asm volatile("st.volatile.global.s32 [%0], %1;" ::"l"(err), "r"(1) : "memory");
 }
-__device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* err, uint32_t ep) {
+// Called by a WHOLE warp: every lane polls the counter (one broadcast load per round) and the exit
+// decision is lane 0's, shuffled, so the warp leaves converged (the named barriers that follow are
+// .aligned).
+__device__ __forceinline__ bool spin_until(const int* c, uint32_t target, int* err, long long t0, int lane) {
+  bool done = !before(ld_acquire(c), target);
+  if (!done && clock64() - t0 > (long long)8000000000LL) {   // ~4 s: deadlock guard -> IOS_ERR_KERNEL
+    if (lane == 0) flag_error(err);
+    done = true;
+  }
+  return __shfl_sync(0xffffffffu, done ? 1 : 0, 0) != 0;
+}
+__device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* err, uint32_t ep, int lane) {
   for (int d = 0; d < P.n_deps; ++d) {
     const int* c = counters + P.dep_idx[d];
     const uint32_t target = (ep + 1u) * (uint32_t)P.dep_target[d];
-    long long t0 = clock64();
-    while (before(ld_acquire(c), target)) {
-      __nanosleep(64);
-      if (clock64() - t0 > (long long)8000000000LL) {   // ~4 s: deadlock guard -> IOS_ERR_KERNEL
-        flag_error(err);
-        break;
-      }
-    }
+    const long long t0 = clock64();
+    while (!spin_until(c, target, err, t0, lane)) __nanosleep(64);
   }
 }
 
 // split-K rendezvous: every split of an output tile arrives after its reductions, then waits for
 // all `n` (the splits of one tile run on distinct, co-resident CTAs; a tile's splits only wait for
 // tiles with higher indices, which the CTAs reach after finishing lower ones: no cycle)
-__device__ __forceinline__ void split_rendezvous(int* ctr, int n, int* err, uint32_t ep) {
-  atom_acqrel_add(ctr, 1);
+__device__ __forceinline__ void split_rendezvous(int* ctr, int n, int* err, uint32_t ep, int lane) {
+  if (lane == 0) atom_acqrel_add(ctr, 1);
+  __syncwarp();
   const uint32_t target = (ep + 1u) * (uint32_t)n;
-  long long t0 = clock64();
-  while (before(ld_acquire(ctr), target)) {
-    __nanosleep(32);
-    if (clock64() - t0 > (long long)8000000000LL) {
-      flag_error(err);
-      break;
-    }
-  }
+  const long long t0 = clock64();
+  while (!spin_until(ctr, target, err, t0, lane)) __nanosleep(32);
 }
 
 // -------------------------------------------------------------------------------- SIMT tile body
@@ -1084,7 +1086,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     for (int t = blockIdx.x; t < sd.n_tiles; t += gridDim.x) {
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
-      if (tid == 0) wait_deps(P, counters, err, ep);
+      if (warp == 0) wait_deps(P, counters, err, ep, lane);
       named_bar(3, kThreads);
 #ifndef IOS_NO_SIMT
       simt_tile<DT>(P, views, t - P.tile_begin, tid, kThreads);
@@ -1115,7 +1117,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const TileCoord tc = tile_coord(P, local);
       const int mt = tc.mt, nt = tc.nt, c0 = tc.c0, c1 = tc.c1;
       if (P.n_deps) {
-        if (ptid == 0) wait_deps(P, counters, err, ep);
+        if (warp == 0) wait_deps(P, counters, err, ep, lane);
         named_bar(1, 128);
       }
       if constexpr ((FEAT & F_FDW) != 0 && DT != ET_F32X) if (P.fdw) {
@@ -1443,7 +1445,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
       if (P.kind != PK_GEMM) {
-        if (etid == 0) wait_deps(P, counters, err, ep);
+        if (warp == kEpilogueWarp0) wait_deps(P, counters, err, ep, lane);
         named_bar(2, 128);
 #ifndef IOS_NO_SIMT
         simt_tile<DT>(P, views, t - P.tile_begin, etid, 128);
@@ -1591,7 +1593,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty[acc]));
           named_bar(2, 128);
-          if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep);
+          if (warp == kEpilogueWarp0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep, lane);
           named_bar(2, 128);
           // distributed finalize: split s owns pixel quads [s*np4/S, (s+1)*np4/S) of the tile; each
           // thread sums its channel's quads over the S slabs (16 float4 in flight) and emits them
@@ -1832,7 +1834,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
         named_bar(2, 128);
         if (etid == 0 && tfirst) IOS_TRACE(13);
-        if (etid == 0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep);
+        if (warp == kEpilogueWarp0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep, lane);
         named_bar(2, 128);
         if (etid == 0 && tfirst) IOS_TRACE(14);
         {
