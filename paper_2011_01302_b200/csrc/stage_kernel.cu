@@ -1574,7 +1574,11 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           float* tacc = reinterpret_cast<float*>(P.workspace) + (int64_t)out_tile * slab * (slabs ? P.split : 1);
           float* trow = tacc + (int64_t)etid * BNx;
           float* mrow = trow + (slabs ? s * slab : 0);
-          for (int c0 = 0; c0 < BNx; c0 += 16) {
+          // the splits of a tile reduce into the same lines: each starts at a different 16-column
+          // round (rotation by split index) so they do not queue on the same L2 lines at once
+          const int nr16 = (BNx + 15) >> 4;
+          for (int k = 0; k < nr16; ++k) {
+            const int c0 = ((k + s) % nr16) * 16;
             uint32_t v[16];
             tmem_ld16(tbase + c0, v);
             tmem_ld_wait();
@@ -1801,7 +1805,11 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         float* macc = tacc + (slabs ? s * slab : 0);            // this split's slab
         const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
         const int wr0 = (warp & 3) * 32;
-        for (int c0 = 0; c0 < BNx; c0 += 32) {
+        // the splits of a tile reduce into the same lines: rotate the 32-column round and the 4-row
+        // group order by split index so they do not queue on the same L2 lines at the same time
+        const int nr32 = (BNx + 31) >> 5;
+        for (int k = 0; k < nr32; ++k) {
+          const int c0 = ((k + s) % nr32) * 32, rot = s;
           uint32_t va[16], vb[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
           acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
@@ -1816,7 +1824,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           __syncwarp();
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
-            const int r = it * 4 + lane / 8, p = lane % 8;
+            const int r = ((it + rot) & 7) * 4 + lane / 8, p = lane % 8;
             uint32_t w0, w1, w2, w3;
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
                          : "r"(stg + r * 128 + ((p ^ (r & 7)) * 16)));
