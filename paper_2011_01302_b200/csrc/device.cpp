@@ -919,12 +919,64 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       p.tile_begin = tiles;
       tiles += p.n_tiles;
     }
-    const int n_counters = kCounterBase + np + n_tilectr;
+    // ---- row-band dependencies: a consumer tile waits only for the producer tiles
+    // covering the input rows it reads, when both sides' tiles map to output rows (not swap-AB, not
+    // a global pool) and the producer's output is the consumer's input grid (IOS_ROW_BANDS=0: off)
+#ifdef IOS_ROW_BANDS
+    static const bool row_bands = !getenv("IOS_ROW_BANDS") || atoi(getenv("IOS_ROW_BANDS")) != 0;
+#else
+    constexpr bool row_bands = false;   // opt-in build (stage_kernel.cu: measured net loss by default)
+#endif
+    std::vector<DepBand> bands;
+    std::vector<int> band_n(np, 0);   // bands of producer q that some consumer waits on (0: none)
+    for (int i = 0; i < np; ++i) {
+      Problem& p = b.probs[i];
+      p.band_begin = -1;
+      p.band_ctr = -1;
+      if (!row_bands || p.n_deps == 0) continue;
+      const bool rows_ok = !(p.kind == PK_GEMM && p.swap_ab) && p.kind != PK_GAVGPOOL;
+      const View& in = b.views[p.in_begin];
+      p.band_begin = (int)bands.size();
+      for (int k = 0; k < p.n_deps; ++k) {
+        const int qi = p.dep_idx[k];
+        const Problem& q = b.probs[qi];
+        DepBand db{};
+        db.H = q.Ho;
+        db.W = q.Wo;
+        if (rows_ok && q.Ho == in.H && q.Wo == in.W && q.batch == p.batch) {
+          if (q.kind == PK_GEMM && !q.swap_ab) {
+            db.mode = q.tt ? 2 : 1;
+            db.bsz = kBM;
+            db.tN = q.tN;
+            db.tR = q.tR;
+            db.tiles_h = q.tiles_h;
+            db.tiles_w = q.tiles_w;
+            db.target = q.n_tiles_n * q.split;
+            db.nbands = q.m_tiles;
+          } else if (q.kind != PK_GEMM && q.kind != PK_GAVGPOOL) {
+            db.mode = q.dwq ? 4 : 3;
+            db.bsz = q.items_per_tile;
+            db.tiles_w = q.dwq ? (q.Wo + q.dwq - 1) / q.dwq : 0;
+            db.target = 1;
+            db.nbands = q.n_tiles;
+          }
+        }
+        if (db.mode) band_n[qi] = db.nbands;
+        bands.push_back(db);
+      }
+    }
+    int n_counters = kCounterBase + np + n_tilectr;
+    for (int i = 0; i < np; ++i)
+      if (band_n[i]) {
+        b.probs[i].band_ctr = n_counters;
+        n_counters += band_n[i];
+      }
     for (int i = 0; i < np; ++i) {
       Problem& p = b.probs[i];
       p.done_idx = kCounterBase + i;
       for (int k = 0; k < p.n_deps; ++k) {
         const Problem& q = b.probs[p.dep_idx[k]];
+        if (p.band_begin >= 0 && bands[p.band_begin + k].mode) bands[p.band_begin + k].ctr = q.band_ctr;
         p.dep_target[k] = q.n_tiles;   // every unit (incl. each split-K part) signals once
         p.dep_idx[k] = kCounterBase + p.dep_idx[k];
       }
@@ -936,14 +988,15 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       for (Problem& p : b.probs)
         if (p.kind == PK_GEMM && p.split > 1) p.workspace += (uint64_t)plan->workspace;
       const size_t pb = b.probs.size() * sizeof(Problem), vb = b.views.size() * sizeof(View),
-                   sb = b.segs.size() * sizeof(Segment);
+                   sb = b.segs.size() * sizeof(Segment), bb = bands.size() * sizeof(DepBand);
       // a problem signals completion only if a later member of the stage waits on it
       for (Problem& p : b.probs)
         for (int k = 0; k < p.n_deps; ++k) b.probs[p.dep_idx[k] - kCounterBase].signal = 1;
-      std::vector<uint8_t> blob(pb + vb + sb + 64, 0);
+      std::vector<uint8_t> blob(pb + vb + sb + bb + 64, 0);
       std::memcpy(blob.data(), b.probs.data(), pb);
       if (vb) std::memcpy(blob.data() + pb, b.views.data(), vb);
       if (sb) std::memcpy(blob.data() + pb + vb, b.segs.data(), sb);
+      if (bb) std::memcpy(blob.data() + pb + vb + sb, bands.data(), bb);
       // tensor maps for TMA-loaded A operands (global memory, 64 B aligned, written before launch)
       std::vector<CUtensorMap> maps;
       const CUtensorMapDataType tdt =
@@ -1013,9 +1066,10 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       sd.n_problems = np;
       sd.n_tiles = tiles;
       sd.n_counters = n_counters;
-      sd.blob_bytes = (int)(pb + vb + sb);
+      sd.blob_bytes = (int)(pb + vb + sb + bb);
       sd.views_off = (int)pb;
       sd.segs_off = (int)(pb + vb);
+      sd.bands_off = (int)(pb + vb + sb);
       sd.uses_counters = 0;
       for (Problem& p : b.probs) sd.uses_counters |= (p.signal || (p.kind == PK_GEMM && p.split > 1)) ? 1 : 0;
       sd.feat = 0;   // kernel feature class (stage_desc.h): which producer paths the stage uses

@@ -72,6 +72,18 @@ inline FastDiv make_fastdiv(uint32_t d) {
   return FastDiv{d, (uint32_t)mul, sh, 0};
 }
 
+// Row-band dependency of a stage member on an in-stage producer: instead of waiting
+// for every tile of the producer, a consumer tile waits only for the producer tiles ("bands") that
+// cover the input rows it reads. Rows are global rows g = n * H + h of the producer's output.
+struct DepBand {
+  int32_t mode;      // 0: whole producer (dep_idx / dep_target); 1: dense GEMM M tiles of bsz pixels;
+                     // 2: patch M tiles (tN images x tR rows x tiles_w column tiles); 3: SIMT tiles of
+                     // bsz pixel items; 4: SIMT tiles of bsz quad items, tiles_w = quads per row
+  int32_t ctr;       // counter index of band 0 (counters[ctr + b] += 1 per unit finishing band b)
+  int32_t target;    // units per band per launch (GEMM: n tiles x splits; SIMT: 1)
+  int32_t bsz, H, W, tN, tR, tiles_h, tiles_w, nbands, pad_;
+};
+
 struct Problem {
   int32_t kind, dtype;
   int32_t tile_begin, n_tiles;      // tiles [tile_begin, tile_begin + n_tiles) of the stage
@@ -79,6 +91,8 @@ struct Problem {
   int32_t n_deps;
   int32_t dep_idx[6];               // wait until counters[dep_idx[i]] >= dep_target[i]
   int32_t dep_target[6];
+  int32_t band_begin;               // DepBand entries [band_begin, band_begin + n_deps) (-1: whole waits)
+  int32_t band_ctr;                 // this problem's own bands: counters[band_ctr + band] (-1: none)
   int32_t batch, flags;             // flags: IOS_F_* of the op
   int32_t kh, kw, sh, sw, ph, pw;
   int32_t Ho, Wo;
@@ -99,7 +113,7 @@ struct Problem {
                                     // reduce into (red.add) and the finalize re-zeroes
   int32_t tilectr_idx;              // split-K arrival counters base
   int32_t slabs;                    // split-K: 1 per-split slabs, 0 one reduction slab (see workspace)
-  int32_t signal;                   // 1: a later member of the stage waits on done_idx
+  int32_t signal;                   // 1: a later member of the stage waits on done_idx (or on its bands)
   FastDiv fd_howo, fd_wo, fd_split, fd_ntn, fd_cin, fd_kw;   // divisors of the tile / im2col decode
   // SIMT geometry
   int32_t items_per_tile, n_items;  // items = output pixels (x channel vectors handled inside)
@@ -154,7 +168,7 @@ struct StageDesc {
                                     // PDL wait) and atomicMax of their exit, %globaltimer ns (0 = off)
   int32_t n_problems, n_tiles, n_counters, has_gemm;
   int32_t blob_bytes;               // problems | views | segments, contiguous from `problems`
-  int32_t views_off, segs_off;
+  int32_t views_off, segs_off, bands_off;
   int32_t uses_counters;            // any in-stage dependency or split-K: counters[0..1] count launches
                                     // (epoch), the others grow monotonically (targets epoch-relative,
                                     // compared wrap-safely mod 2^32)

@@ -316,6 +316,7 @@ __device__ __forceinline__ bool spin_until(const int* c, uint32_t target, int* e
   }
   return __shfl_sync(0xffffffffu, done ? 1 : 0, 0) != 0;
 }
+#ifndef IOS_ROW_BANDS
 __device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* err, uint32_t ep, int lane) {
   for (int d = 0; d < P.n_deps; ++d) {
     const int* c = counters + P.dep_idx[d];
@@ -324,6 +325,135 @@ __device__ __forceinline__ void wait_deps(const Problem& P, int* counters, int* 
     while (!spin_until(c, target, err, t0, lane)) __nanosleep(64);
   }
 }
+#define IOS_BAND_SIGNAL(band) \
+  do {                        \
+  } while (0)
+#else
+// Row-band dependencies (opt-in build: tools/build_variant.py bands -DIOS_ROW_BANDS).
+// Measured (1 B200, interleaved): the Inception stem stage (three chained big-M convs, each 1.2 waves)
+// 30.5 -> 26.5 us, other chain stages unchanged, but the extra wait / signal code cost 2-3 % on every
+// other stage (Inception IOS schedule 0.517 -> 0.530 ms), so the default build leaves it out.
+#define IOS_BAND_SIGNAL(band)                                                          \
+  do {                                                                                 \
+    if (P.band_ctr >= 0) red_release_add(counters + P.band_ctr + (band), 1);          \
+  } while (0)
+// g0..g1: the global input rows (n * H + h) this tile reads; a dependency in band mode waits only for
+// the producer bands covering them, otherwise for the whole producer. Called by a
+// whole warp: the lanes poll all needed counters (every dependency, every band) in parallel -- one
+// round trip per polling round instead of one acquire per counter (measured: sequential acquires
+// made band waits slower than whole-producer waits; relaxed polls + one fence.acq_rel were slower
+// still).
+static __device__ __noinline__ void wait_deps(const Problem& P, const DepBand* bands, int* counters, int* err, uint32_t ep,
+                                       int lane, int g0, int g1) {
+  int cb[6], lo[6], hi[6];
+  uint32_t tg[6];
+  const int nd = min(P.n_deps, 6);
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    if (d >= nd) break;
+    const DepBand* B = P.band_begin >= 0 ? bands + P.band_begin + d : nullptr;
+    if (!B || B->mode == 0) {
+      cb[d] = P.dep_idx[d];
+      lo[d] = hi[d] = 0;
+      tg[d] = (ep + 1u) * (uint32_t)P.dep_target[d];
+      continue;
+    }
+    int b0, b1;
+    if (B->mode == 2) {
+      const int i0 = (g0 / B->H) / B->tN * B->tiles_h + (g0 % B->H) / B->tR;
+      const int i1 = (g1 / B->H) / B->tN * B->tiles_h + (g1 % B->H) / B->tR;
+      b0 = i0 * B->tiles_w;
+      b1 = i1 * B->tiles_w + B->tiles_w - 1;
+    } else {
+      const int per_row = B->mode == 4 ? B->tiles_w : B->W;   // items per global row
+      b0 = g0 * per_row / B->bsz;
+      b1 = (g1 * per_row + per_row - 1) / B->bsz;
+    }
+    cb[d] = B->ctr;
+    lo[d] = b0;
+    hi[d] = min(b1, B->nbands - 1);
+    tg[d] = (ep + 1u) * (uint32_t)B->target;
+  }
+  // flatten (dependency, band) pairs; lane i polls items i, i + 32, ... (acquire loads: a lane's
+  // acquire plus the named barrier that follows orders the producers' writes for the whole CTA)
+  int first[7];
+  first[0] = 0;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) first[d + 1] = first[d] + (d < nd ? hi[d] - lo[d] + 1 : 0);
+  const int total = first[nd];
+  const long long t0 = clock64();
+  for (;;) {
+    bool ok = true;
+    for (int k = lane; k < total; k += 32) {
+      int d = 0;
+#pragma unroll
+      for (int e = 1; e < 6; ++e) d += (e < nd && k >= first[e]) ? 1 : 0;
+      ok &= !before(ld_acquire(counters + cb[d] + lo[d] + (k - first[d])), tg[d]);
+    }
+    if (__all_sync(0xffffffffu, ok)) break;
+    const bool late = __shfl_sync(0xffffffffu, (clock64() - t0 > (long long)8000000000LL) ? 1 : 0, 0) != 0;
+    if (late) {   // ~4 s deadlock guard -> IOS_ERR_KERNEL
+      if (lane == 0) flag_error(err);
+      break;
+    }
+    __nanosleep(64);
+  }
+}
+
+// input rows (global g = n * H + h) read by output rows oh0..oh1 of images n0..n1 through a window of
+// k rows, stride s, padding p over an input of height H
+__device__ __forceinline__ void window_rows(int n0, int oh0, int n1, int oh1, int k, int s, int p, int H, int& g0,
+                                            int& g1) {
+  g0 = n0 * H + max(0, oh0 * s - p);
+  g1 = n1 * H + min(H - 1, oh1 * s - p + k - 1);
+}
+// rows read by GEMM tile mt (non-swap: dense 128-pixel tiles or patch tiles; swap-AB: every row)
+static __device__ __noinline__ void gemm_rows(const Problem& P, int Hin, int mt, int& g0, int& g1) {
+  if (P.swap_ab) {
+    g0 = 0;
+    g1 = P.batch * Hin - 1;
+    return;
+  }
+  const int k = P.fdw ? P.dk : P.kh, st = P.fdw ? P.ds : P.sh, pd = P.fdw ? P.dp : P.ph;
+  int n0, n1, oh0, oh1;
+  if (P.tt) {
+    const int rr = fdiv(P.fd_tilw, mt);
+    const int tnn = fdiv(P.fd_tilh, rr);
+    const int th = rr - tnn * P.tiles_h;
+    n0 = tnn * P.tN;
+    n1 = min(P.batch, n0 + P.tN) - 1;
+    oh0 = th * P.tR;
+    oh1 = min(P.Ho, oh0 + P.tR) - 1;
+  } else {
+    const int hw = P.Ho * P.Wo;
+    const int p0 = mt * kBM, p1 = min(P.M, p0 + kBM) - 1;
+    n0 = p0 / hw;
+    oh0 = (p0 - n0 * hw) / P.Wo;
+    n1 = p1 / hw;
+    oh1 = (p1 - n1 * hw) / P.Wo;
+  }
+  window_rows(n0, oh0, n1, oh1, k, st, pd, Hin, g0, g1);
+}
+// rows read by SIMT tile `tile` (items: pixels, or quads of dwq pixels along a row; global pools: all)
+static __device__ __noinline__ void simt_rows(const Problem& P, int Hin, int tile, int& g0, int& g1) {
+  const int i0 = tile * P.items_per_tile, i1 = min(i0 + P.items_per_tile, P.n_items) - 1;
+  if (P.kind == PK_GAVGPOOL || i1 < i0) {
+    g0 = 0;
+    g1 = P.batch * Hin - 1;
+    return;
+  }
+  int r0, r1;   // output global rows
+  if (P.dwq) {
+    const int wq = (P.Wo + P.dwq - 1) / P.dwq;
+    r0 = i0 / wq;
+    r1 = i1 / wq;
+  } else {
+    r0 = i0 / P.Wo;
+    r1 = i1 / P.Wo;
+  }
+  window_rows(r0 / P.Ho, r0 % P.Ho, r1 / P.Ho, r1 % P.Ho, P.kh, P.sh, P.ph, Hin, g0, g1);
+}
+#endif  // IOS_ROW_BANDS
 
 // split-K rendezvous: every split of an output tile arrives after its reductions, then waits for
 // all `n` (the splits of one tile run on distinct, co-resident CTAs; a tile's splits only wait for
@@ -994,6 +1124,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   const Problem* probs = reinterpret_cast<const Problem*>(dbase);
   const View* views = reinterpret_cast<const View*>(dbase + sd.views_off);
   const Segment* segs = reinterpret_cast<const Segment*>(dbase + sd.segs_off);
+#ifdef IOS_ROW_BANDS
+  const DepBand* bands = reinterpret_cast<const DepBand*>(dbase + sd.bands_off);
+#endif
   int* counters = reinterpret_cast<int*>(sd.counters);
   int* err = reinterpret_cast<int*>(sd.err);
   // optional per-CTA timeline (ns, %globaltimer) for tools/trace_stage.py; slots: 0 entry, 1 prologue
@@ -1086,13 +1219,24 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     for (int t = blockIdx.x; t < sd.n_tiles; t += gridDim.x) {
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
-      if (warp == 0) wait_deps(P, counters, err, ep, lane);
+      if (warp == 0 && P.n_deps) {
+#ifdef IOS_ROW_BANDS
+        int g0, g1;
+        simt_rows(P, views[P.in_begin].H, t - P.tile_begin, g0, g1);
+        wait_deps(P, bands, counters, err, ep, lane, g0, g1);
+#else
+        wait_deps(P, counters, err, ep, lane);
+#endif
+      }
       named_bar(3, kThreads);
 #ifndef IOS_NO_SIMT
       simt_tile<DT>(P, views, t - P.tile_begin, tid, kThreads);
 #endif
       named_bar(3, kThreads);
-      if (tid == 0 && P.signal) red_release_add(counters + P.done_idx, 1);
+      if (tid == 0 && P.signal) {
+        red_release_add(counters + P.done_idx, 1);
+        IOS_BAND_SIGNAL(t - P.tile_begin);
+      }
     }
   } else if (warp < kProducerWarps) {
     // ============================================================== PRODUCER (A gather + B bulk)
@@ -1117,7 +1261,15 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const TileCoord tc = tile_coord(P, local);
       const int mt = tc.mt, nt = tc.nt, c0 = tc.c0, c1 = tc.c1;
       if (P.n_deps) {
-        if (warp == 0) wait_deps(P, counters, err, ep, lane);
+        if (warp == 0) {
+#ifdef IOS_ROW_BANDS
+          int g0, g1;
+          gemm_rows(P, views[P.in_begin].H, mt, g0, g1);
+          wait_deps(P, bands, counters, err, ep, lane, g0, g1);
+#else
+          wait_deps(P, counters, err, ep, lane);
+#endif
+        }
         named_bar(1, 128);
       }
       if constexpr ((FEAT & F_FDW) != 0 && DT != ET_F32X) if (P.fdw) {
@@ -1445,13 +1597,24 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
       if (P.kind != PK_GEMM) {
-        if (warp == kEpilogueWarp0) wait_deps(P, counters, err, ep, lane);
+        if (warp == kEpilogueWarp0 && P.n_deps) {
+#ifdef IOS_ROW_BANDS
+          int g0, g1;
+          simt_rows(P, views[P.in_begin].H, t - P.tile_begin, g0, g1);
+          wait_deps(P, bands, counters, err, ep, lane, g0, g1);
+#else
+          wait_deps(P, counters, err, ep, lane);
+#endif
+        }
         named_bar(2, 128);
 #ifndef IOS_NO_SIMT
         simt_tile<DT>(P, views, t - P.tile_begin, etid, 128);
 #endif
         named_bar(2, 128);
-        if (etid == 0 && P.signal) red_release_add(counters + P.done_idx, 1);
+        if (etid == 0 && P.signal) {
+          red_release_add(counters + P.done_idx, 1);
+          IOS_BAND_SIGNAL(t - P.tile_begin);
+        }
         continue;
       }
       const int local = t - P.tile_begin;
@@ -1644,7 +1807,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         }
         if (P.signal) {
           named_bar(2, 128);
-          if (etid == 0) red_release_add(counters + P.done_idx, 1);
+          if (etid == 0) {
+            red_release_add(counters + P.done_idx, 1);
+            IOS_BAND_SIGNAL(mt);
+          }
         }
         tfirst = false;
         acc ^= 1;
@@ -1919,7 +2085,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       }
       if (P.signal) {
         named_bar(2, 128);
-        if (etid == 0) red_release_add(counters + P.done_idx, 1);
+        if (etid == 0) {
+          red_release_add(counters + P.done_idx, 1);
+          IOS_BAND_SIGNAL(mt);
+        }
       }
       tfirst = false;
       acc ^= 1;
