@@ -1866,24 +1866,22 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
       const int out_tile = mt * P.n_tiles_n + nt;
-      if (P.split == 1 && P.n_seg == 1) {
-        // one output segment (every non-merged GEMM). Per 32-column round: TMEM -> registers
-        // (thread = row) -> bias/ReLU/rounding -> this warp's 4 KB smem staging tile (16 B pieces
-        // XOR-swizzled by row: conflict-free) -> coalesced 16 B global stores (lanes sweep a row's
-        // contiguous channels; 4 rows per instruction) instead of 32 scattered rows.
+      if (P.split == 1) {
+        // Per 32-column round: TMEM -> registers (thread = row) -> bias/rounding -> this warp's 4 KB
+        // smem staging tile (16 B pieces XOR-swizzled by row: conflict-free) -> coalesced 16 B global
+        // stores (lanes sweep a row's contiguous channels; 4 rows per instruction) instead of 32
+        // scattered rows. A merged conv's columns belong to several output segments (branches,
+        // P:193 split): segments are multiples of 8 channels, so every 16 B piece lies in one segment;
+        // each lane looks up its piece's segment once per round and applies that branch's ReLU
+        // (after rounding: max(0, rnd(x)) == rnd(max(0, x)) for TF32 and bf16).
         constexpr int OESZ = DT == ET_BF16 ? 2 : 4;
         constexpr int PPR = 32 * OESZ / 16;                 // 16 B pieces per row per round (8 / 4)
-        const Segment& sg = segs[P.seg_begin];
-        const int relu = sg.relu;
-        const int ncols = min(BNx, sg.n1 - nt * BNx);     // valid columns of this tile
-        char* obase = reinterpret_cast<char*>(sg.out.ptr) +
-                      ((int64_t)sg.out.coff + nt * BNx - sg.n0) * OESZ;
-        const int ocs = sg.out.cstride;
         const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
         constexpr int RPI = 32 / PPR;                       // rows per write-out instruction (4 / 8)
         int opix[32 / RPI];                                 // output pixel of each row this lane writes
 #pragma unroll
         for (int it = 0; it < 32 / RPI; ++it) opix[it] = pixel((warp & 3) * 32 + it * RPI + lane / PPR);
+        const int sg0 = P.seg_begin, nsg = P.n_seg;
         for (int c0 = 0; c0 < BNx; c0 += 32) {
           uint32_t va[16], vb[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
@@ -1892,10 +1890,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(13);
           float o[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            o[e] = __uint_as_float(e < 16 ? va[e] : vb[e - 16]) + sbias[c0 + e];
-            if (relu) o[e] = fmaxf(o[e], 0.f);
-          }
+          for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(e < 16 ? va[e] : vb[e - 16]) + sbias[c0 + e];
 #pragma unroll
           for (int p = 0; p < PPR; ++p) {
             uint32_t w[4];
@@ -1914,49 +1909,43 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           }
           __syncwarp();
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(14);
+          // this lane's piece column and its segment (destination, channel stride, ReLU)
+          const int p = lane % PPR;
+          const int ncol = nt * BNx + c0 + p * (16 / OESZ);
+          char* dst = nullptr;
+          int ocs = 0, relu = 0;
+          // (columns past BN in the last round belong to the next N tile: never written from here)
+          for (int q = 0; q < nsg && c0 + p * (16 / OESZ) < BNx; ++q) {
+            const Segment& sg = segs[sg0 + q];
+            if (ncol >= sg.n0 && ncol < sg.n1) {
+              dst = reinterpret_cast<char*>(sg.out.ptr) + ((int64_t)sg.out.coff + ncol - sg.n0) * OESZ;
+              ocs = sg.out.cstride;
+              relu = sg.relu;
+            }
+          }
           // coalesced write-out: lane -> (row, piece)
 #pragma unroll
           for (int it = 0; it < 32 / RPI; ++it) {
-            const int r = it * RPI + lane / PPR, p = lane % PPR;
-            uint32_t w0, w1, w2, w3;
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+            const int r = it * RPI + lane / PPR;
+            uint32_t w[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
                          : "r"(stg + r * (PPR * 16) + ((p ^ (r & 7)) % PPR) * 16));
-            const int col = c0 + p * (16 / OESZ);
-            if (opix[it] >= 0 && col < ncols)
-              stg_v4(obase + ((int64_t)opix[it] * ocs + col) * OESZ, w0, w1, w2, w3);
+            if (relu) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (DT == ET_BF16) {
+                  __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&w[q]);
+                  h = __hmax2(h, __floats2bfloat162_rn(0.f, 0.f));
+                  w[q] = *reinterpret_cast<uint32_t*>(&h);
+                } else {
+                  w[q] = __float_as_uint(fmaxf(__uint_as_float(w[q]), 0.f));
+                }
+              }
+            }
+            if (opix[it] >= 0 && dst) stg_v4(dst + (int64_t)opix[it] * ocs * OESZ, w[0], w[1], w[2], w[3]);
           }
           __syncwarp();
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(15);
-        }
-        tc_fence_before();
-        if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
-      } else if (P.split == 1) {
-        for (int c0 = 0; c0 < BNx; c0 += 16) {
-          uint32_t v[16];
-          acc_ld16<DT>(tbase + c0, sacc, c0, v);
-          acc_wait<DT>();
-          if (!valid) continue;
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            const int ncol = nt * BNx + c0 + g * 8;
-            for (int q = 0; q < P.n_seg; ++q) {
-              const Segment& sg = segs[P.seg_begin + q];
-              if (ncol >= sg.n0 && ncol < sg.n1) {
-                float o[8];
-                const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + ncol));
-                const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + ncol + 4));
-                const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  o[e] = __uint_as_float(v[g * 8 + e]) + bb[e];
-                  if (sg.relu) o[e] = fmaxf(o[e], 0.f);
-                }
-                store_vec(sg.out, P.dtype, m, ncol - sg.n0, o);
-                if (esz_out == 4) store_vec(sg.out, P.dtype, m, ncol - sg.n0 + 4, o + 4);
-                break;
-              }
-            }
-          }
         }
         tc_fence_before();
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
