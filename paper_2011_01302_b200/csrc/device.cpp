@@ -37,6 +37,7 @@ struct OpDev {
   float* add_w = nullptr;     // add / sepconv aggregation weights
   View dw_out{};              // sepconv depthwise scratch (NHWC, Cp_in channels)
   int tt = 0, kblk = 0;       // weights packed for the tap-TMA im2col path (K = taps x kblk blocks)
+  int unfold = 0;             // reads the W-unfolded graph input (DeviceState::unfold): kernel kh x 1
 };
 
 }  // namespace
@@ -69,6 +70,14 @@ struct DeviceState {
   std::map<std::tuple<int, uint64_t, int>, int> tile_variant;
   std::vector<StagePlan*> retired;   // plans replaced by tuning (a captured schedule may use them)
   uint64_t plan_gen = 0;             // bumped when tuning replaces plans: captured schedules re-capture
+  // W-unfolded copy of the graph input for a narrow first conv (Cin*esz < 64 B, kw > 1): pixel
+  // (n, h, ow) holds the kw input pixels the conv's output column ow reads along W, channel
+  // j * C + c = x[n, h, ow*sw - pw + j, c] (zero outside), padded to one 128 B block. The conv then
+  // runs as a kh x 1 conv with stride (sh, 1) on the tap-TMA path: dense 128 B taps instead of a
+  // 16 B-granular gather (measured: SqueezeNet conv1 7x7/2 at batch 128 was 37 % of the network).
+  bool unfold = false;
+  View unfold_view{};
+  int unfold_kw = 0, unfold_sw = 1, unfold_pw = 0;
 };
 
 namespace {
@@ -303,6 +312,28 @@ void ensure_device(Graph& g) {
       d.od[v].elided = true;
     }
   }
+  // ---- W-unfolded graph input (at most one narrow first conv may use it; others read op 0 as is)
+  {
+    static const bool on = !getenv("IOS_UNFOLD") || atoi(getenv("IOS_UNFOLD")) != 0;
+    const int elems = kChunkBytes / g.esize();
+    for (int v = 1; v < n && on && g.math != IOS_MATH_FP32_SIMT; ++v) {
+      const Op& o = g.ops[v];
+      const Op& x = g.ops[0];
+      if (o.kind != IOS_OP_CONV || o.inputs[0] != 0 || (o.flags & IOS_F_RELU_PRE)) continue;
+      if (x.Cp * g.esize() >= 64 || o.kw < 2 || o.sw > o.kw || o.kw * x.C > elems) continue;
+      // worth its extra layout launch only for large outputs (measured at batch 1, Inception V3's
+      // 149x149 stem conv: +0.3 % end to end; SqueezeNet conv1 at batch 128: 984 -> 332 us)
+      if ((int64_t)o.N * o.H * o.W < 65536) continue;
+      void* p = dmalloc(d, (size_t)x.N * x.H * o.W * elems * g.esize());
+      d.unfold = true;
+      d.unfold_view = View{(uint64_t)p, elems, 0, elems, o.kw * x.C, x.H, o.W};
+      d.unfold_kw = o.kw;
+      d.unfold_sw = o.sw;
+      d.unfold_pw = o.pw;
+      d.od[v].unfold = 1;
+      break;
+    }
+  }
   // ---- weights
   const int wdt = g.dtype();
   for (int v = 1; v < n; ++v) {
@@ -310,7 +341,23 @@ void ensure_device(Graph& g) {
     OpDev& e = d.od[v];
     const Op& x = g.ops[o.inputs[0]];
     if (!o.add_w.empty()) e.add_w = upload(d, o.add_w);
-    if (o.kind == IOS_OP_CONV || o.kind == IOS_OP_LINEAR) {
+    if (o.kind == IOS_OP_CONV && e.unfold) {
+      // kh x 1 conv over the unfolded input: K = kh taps x one 128 B block, channel j * C + c of
+      // tap i holds W[co][c][i][j]
+      const int cin = x.C, kh = o.kh, kw = o.kw, elems = kChunkBytes / g.esize();
+      const float* W = o.weight.data();
+      e.kblk = 1;
+      e.tt = 1;
+      e.wpack = pack_gemm(d, o.Cp, kh * elems, wdt, [&](int nn, int k) -> float {
+        if (nn >= o.cout) return 0.0f;
+        const int i = k / elems, ch = k % elems;
+        if (ch >= kw * cin) return 0.0f;
+        const int j = ch / cin, c = ch % cin;
+        return W[(((size_t)nn * cin + c) * kh + i) * kw + j];
+      }, &e.wpack_n8);
+      std::vector<float> b(o.bias);
+      e.bias = upload(d, b, (size_t)round_up(o.Cp, 256) + 16);
+    } else if (o.kind == IOS_OP_CONV || o.kind == IOS_OP_LINEAR) {
       const int cin = x.C, cin_p = x.Cp, kh = o.kh, kw = o.kw;
       const float* W = o.weight.data();
       // tap-TMA im2col packs K per tap in whole 128 B channel blocks (zero rows for the padding)
@@ -735,8 +782,10 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
           case IOS_OP_CONV:
           case IOS_OP_LINEAR: {
             const int u = o.inputs[0];
-            const int pi = b.gemm(u, d.od[u].out, e.wpack, e.wpack_n8, e.bias, o.Cp, o.kh, o.kw, o.sh, o.sw, o.ph, o.pw,
-                                  o.H, o.W, o.flags & IOS_F_RELU_PRE, e.kblk);
+            const int pi = e.unfold ? b.gemm(u, d.unfold_view, e.wpack, e.wpack_n8, e.bias, o.Cp, o.kh, 1, o.sh, 1, o.ph, 0,
+                                             o.H, o.W, 0, 1)
+                                    : b.gemm(u, d.od[u].out, e.wpack, e.wpack_n8, e.bias, o.Cp, o.kh, o.kw, o.sh, o.sw, o.ph,
+                                             o.pw, o.H, o.W, o.flags & IOS_F_RELU_PRE, e.kblk);
             b.seg(pi, 0, o.Cp, e.out, (o.flags & IOS_F_RELU_POST) ? 1 : 0);
             b.add_deps(pi, deps);
             b.op_probs[v] = {pi};
@@ -1443,6 +1492,11 @@ void run_schedule(Graph& g, Schedule& q, const void* d_in, void* d_out, cudaStre
     int launches = 0;
     cudaError_t e = launch_nchw_to_nhwc(static_cast<const float*>(d_in), d.od[0].out, g.dtype(), in.N, in.C, d.stream);
     ++launches;
+    if (e == cudaSuccess && d.unfold) {
+      e = launch_nchw_unfold(static_cast<const float*>(d_in), d.unfold_view, g.dtype(), in.N, in.C, in.W, d.unfold_kw,
+                             d.unfold_sw, d.unfold_pw, d.stream);
+      ++launches;
+    }
     for (StagePlan* p : plans) {
       if (e != cudaSuccess) break;
       if (p->empty) continue;
@@ -1509,6 +1563,9 @@ void run_timeline(Graph& g, Schedule& q, const void* d_in, void* d_out, int reps
     }
     const Op& in = g.ops[0];
     IOS_CHECK_CUDA(launch_nchw_to_nhwc(static_cast<const float*>(d_in), d.od[0].out, g.dtype(), in.N, in.C, d.stream));
+    if (d.unfold)
+      IOS_CHECK_CUDA(launch_nchw_unfold(static_cast<const float*>(d_in), d.unfold_view, g.dtype(), in.N, in.C, in.W,
+                                        d.unfold_kw, d.unfold_sw, d.unfold_pw, d.stream));
     for (int i = 0; i < n; ++i) {
       if (plans[i]->empty) continue;
       StageDesc sd = plans[i]->sd;
@@ -1584,7 +1641,7 @@ void load_tile_variants(Graph& g, const std::string& path) {
 
 int schedule_launches(Graph& g, Schedule& q) {
   ensure_device(g);
-  int n = 2;
+  int n = 2 + (g.dev->unfold ? 1 : 0);
   for (const Stage& s : q.stages) {
     int bpos = -1;
     const uint64_t mask = g.mask_of(s.ops, &bpos);

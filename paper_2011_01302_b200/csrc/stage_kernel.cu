@@ -2143,6 +2143,30 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ in, View out, int 
   }
 }
 
+// NCHW fp32 (caller) -> the W-unfolded NHWC input of a narrow first conv (DeviceState::unfold):
+// out pixel (n, h, ow), channel j * C + c = in[n, c, h, ow*sw - pw + j] (0 outside the image and in
+// the padding channels), rounded to the storage precision.
+__global__ void nchw_unfold_kernel(const float* __restrict__ in, View out, int dtype, int N, int C, int W, int kw, int sw,
+                                   int pw) {
+  const int64_t total = (int64_t)N * out.H * out.W * out.C;
+  const int64_t hw = (int64_t)out.H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % out.C);
+    const int64_t pix = i / out.C;
+    const int ow = (int)(pix % out.W);
+    const int64_t nh = pix / out.W;
+    const int h = (int)(nh % out.H);
+    const int64_t n = nh / out.H;
+    float x = 0.f;
+    if (ch < kw * C) {
+      const int j = ch / C, c = ch - (ch / C) * C;
+      const int w = ow * sw - pw + j;
+      if (w >= 0 && w < W) x = in[(n * C + c) * hw + (int64_t)h * W + w];
+    }
+    store_elem(out, dtype, pix, ch, x);
+  }
+}
+
 __global__ void nhwc_to_nchw_kernel(View in, int dtype, float* __restrict__ out, int N, int C) {
   const int64_t hw = (int64_t)in.H * in.W;
   const int64_t total = (int64_t)N * C * hw;
@@ -2218,6 +2242,15 @@ cudaError_t launch_nchw_to_nhwc(const float* in, const View& out, int dtype, int
   const int64_t total = (int64_t)N * out.H * out.W * out.C;
   int64_t g64 = (total + 255) / 256; int grid = (int)(g64 < 148 * 8 ? g64 : 148 * 8);
   nchw_to_nhwc_kernel<<<grid, 256, 0, st>>>(in, out, dtype, N, C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nchw_unfold(const float* in, const View& out, int dtype, int N, int C, int W, int kw, int sw, int pw,
+                               cudaStream_t st) {
+  const int64_t total = (int64_t)N * out.H * out.W * out.C;
+  int64_t g64 = (total + 255) / 256;
+  int grid = (int)(g64 < 148 * 8 ? g64 : 148 * 8);
+  nchw_unfold_kernel<<<grid, 256, 0, st>>>(in, out, dtype, N, C, W, kw, sw, pw);
   return cudaGetLastError();
 }
 

@@ -19,9 +19,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--net", default="inception_v3")
 ap.add_argument("--schedule", default="ios")
 ap.add_argument("--tune", type=int, default=1)
+ap.add_argument("--batch", type=int, default=1)
 a = ap.parse_args()
 math = NETS[a.net]["math"]
-net = W.build(a.net, math=math)
+net = W.build(a.net, math=math, batch=a.batch)
 g = Graph.from_netspec(net, math)
 q = {"ios": lambda: g.schedule_dp(3, 8), "seq": g.schedule_sequential, "greedy": g.schedule_greedy}[a.schedule]()
 if a.tune:
@@ -36,7 +37,8 @@ prof = [g.stage_latency(ops, t) * 1e3 if ops and net.op(ops[0]).kind != "concat"
 rows = stage_roofline(g, net, q, _peaks(), times_ms=[c[2] * 1e-3 for c in cold])
 print(f"{'i':>3s} {'prof':>7s} {'warm':>7s} {'cold':>7s} {'span':>7s} {'roof':>6s}  ops")
 for i, ((ops, t, _), p, w, c, r) in enumerate(zip(q.stages, prof, warm, cold, rows)):
-    print(f"{i:3d} {p:7.2f} {w[2]:7.2f} {c[2]:7.2f} {c[1]-c[0]:7.2f} {r['roof_ms']*1e3:6.2f}  {ops}")
+    print(f"{i:3d} {p:7.2f} {w[2]:7.2f} {c[2]:7.2f} {c[1]-c[0]:7.2f} {r['roof_ms']*1e3:6.2f} {r['bound']:6s} "
+          f"F={r['flops']/1e9:6.2f}G B={r['bytes']/1e6:7.1f}MB  {ops} {[net.op(v).name for v in ops][:3]}")
 P, Wm, Cd = sum(prof), sum(w[2] for w in warm), sum(c[2] for c in cold)
 print(f"sum: profiled {P:.1f} us, in-run warm {Wm:.1f} us, in-run L2-flushed {Cd:.1f} us, roof {sum(r['roof_ms'] for r in rows)*1e3:.1f} us")
 nz = [(p, c[2]) for p, c in zip(prof, cold) if p > 0]
