@@ -224,7 +224,9 @@ int tap_tma_blocks(const Graph& g, int cin_p, int kh, int kw, int sh, int sw, in
   if (sh > 8 || sw > 8) return 0;
   const int elems = kChunkBytes / g.esize();
   const int kblk = (cin_p + elems - 1) / elems;
-  if (cin_p < 16 || kblk * elems * 2 > cin_p * 3) return 0;   // at most 1.5x K padding
+  // at most 1.5x K padding by default (IOS_TT_PAD2 = twice the allowed ratio: 3 -> 1.5x, 4 -> 2x)
+  static const int pad2 = getenv("IOS_TT_PAD2") ? atoi(getenv("IOS_TT_PAD2")) : 3;
+  if (cin_p < 16 || kblk * elems * 2 > cin_p * pad2) return 0;
   const int64_t dense = ((int64_t)batch * Ho * Wo + kBM - 1) / kBM;
   if ((int64_t)tt_geometry(batch, Ho, Wo, sh, sw).tiles * 4 > dense * 5) return 0;
   return kblk;
@@ -1372,8 +1374,11 @@ void measure_stages(Graph& g, int bpos, const std::vector<std::pair<uint64_t, in
   DeviceState& d = *g.dev;
   // 3 trials x 10 back-to-back launches per stage: with 3 x 3 the DP's choices between schedules
   // whose totals differed by ~1 % were decided by event-timer noise (SqueezeNet r1: DP 165 us vs
-  // greedy 160 us when re-measured with the full protocol). IOS_SEARCH_REPS overrides.
-  static const int kReps = getenv("IOS_SEARCH_REPS") ? std::max(1, atoi(getenv("IOS_SEARCH_REPS"))) : 10;
+  // greedy 160 us when re-measured with the full protocol). Blocks with more than 5000 candidate
+  // stages (NASNet cells, RandWire stages) keep 3 launches, bounding the search time; the measured
+  // refinement (ios_schedule_refine) re-checks the result in context. IOS_SEARCH_REPS overrides.
+  static const int env_reps = getenv("IOS_SEARCH_REPS") ? std::max(1, atoi(getenv("IOS_SEARCH_REPS"))) : 0;
+  const int kReps = env_reps ? env_reps : (stages.size() > 5000 ? 3 : 10);
   constexpr int kBatch = 48, kTrials = 3;
   const uint64_t sig = g.block_sig(bpos);
   std::vector<cudaEvent_t> ev;
