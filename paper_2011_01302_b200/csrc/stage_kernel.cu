@@ -1198,16 +1198,20 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     }
   }
 #endif
+  // launch epoch: every CTA of a launch adds 1 to the launch counter exactly once, before releasing the
+  // next launch (launch_dependents), so old / grid is this launch's number for every CTA
+  // (64-bit, in counters[0..1]: it never wraps; the epoch itself is used mod 2^32). The counters are
+  // the plan's own, and every CTA of an earlier launch of this plan added its 1 before that launch
+  // triggered its dependents, so the add is issued BEFORE the PDL wait: its L2 round trip overlaps
+  // the previous grid's tail instead of delaying every role after the wait.
+  unsigned long long ep_old = 0;
+  if (sd.uses_counters && tid == 0) ep_old = atomicAdd(reinterpret_cast<unsigned long long*>(counters), 1ull);
   // programmatic dependent launch: the prologue above overlapped the previous stage's tail; from
   // here on we read activations (and counters) the previous grid may still be writing
   if (tid == 0) IOS_TRACE(11);   // before waiting for the previous grid
   pdl_wait();
   if (sd.stamp && tid == 0) atomicMin(reinterpret_cast<unsigned long long*>(sd.stamp), (unsigned long long)gtimer());
-  // launch epoch: every CTA of a launch adds 1 to the launch counter exactly once, before releasing the
-  // next launch (launch_dependents), so old / grid is this launch's number for every CTA
-  // (64-bit, in counters[0..1]: it never wraps; the epoch itself is used mod 2^32)
-  if (sd.uses_counters && tid == 0)
-    *flag = (int)(uint32_t)(atomicAdd(reinterpret_cast<unsigned long long*>(counters), 1ull) / gridDim.x);
+  if (sd.uses_counters && tid == 0) *flag = (int)(uint32_t)(ep_old / gridDim.x);
   pdl_launch_dependents();
   named_bar(4, kThreads);
   const uint32_t ep = sd.uses_counters ? (uint32_t)*flag : 0u;
