@@ -55,8 +55,9 @@ def build(force: bool = False, verbose: bool = False, extra_defs=(), out: str = 
     units = [(src, []) for src in SOURCES]
     # (dtype, smem-descriptor, feature class): TF32 / BF16 x {lean, gather, full, trace}; FP32-SIMT x
     # {full, trace} (stage_kernel.cu launch_stage, stage_desc.h KernelFeature)
-    insts = [(dt, sdv, ft) for dt in (0, 1) for sdv in (0, 1) for ft in (0, 1, 3, 7)]
-    insts += [(2, sdv, ft) for sdv in (0, 1) for ft in (3, 7)]
+    # + the cluster split-K classes (F_CSK = 8: lean / gather / full) and the trace class (all features)
+    insts = [(dt, sdv, ft) for dt in (0, 1) for sdv in (0, 1) for ft in (0, 1, 3, 8, 9, 11, 15)]
+    insts += [(2, sdv, ft) for sdv in (0, 1) for ft in (3, 15)]
     units += [("stage_kernel.cu", [f"-DIOS_INST_DT={dt}", f"-DIOS_INST_SD={sdv}", f"-DIOS_INST_FEAT={ft}"])
               for dt, sdv, ft in insts]
     for src, defs in units:

@@ -58,6 +58,7 @@ struct StagePlan {
 struct DeviceState {
   bool ready = false;
   int num_sms = 148;
+  int cluster_ctas = 0;              // co-resident CTAs of a cluster-split-K launch (stage_cluster_ctas)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<OpDev> od;
@@ -245,6 +246,7 @@ void ensure_device(Graph& g) {
   if (prop.major != 10 || prop.minor != 0)
     IOS_FAIL(IOS_ERR_CUDA, std::string("libios is built for sm_100a; device is ") + prop.name);
   d.num_sms = prop.multiProcessorCount;
+  d.cluster_ctas = stage_cluster_ctas() / kClusterCtas * kClusterCtas;
   IOS_CHECK_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
   {
     cudaMemPool_t pool;
@@ -514,13 +516,19 @@ static TileKnobs tile_knobs() {
 }
 
 // Tiling variants the stage tuner (ios_schedule_tune) may pick per stage: 0 = the default knobs,
-// 1 = finer split-K (>= 2 chunks per unit), 2 = coarser split-K (>= 8 chunks per unit). Measured:
-// the best split-K granularity differs by network and stage (profiles/r1_kernel_ab_findings.md §5).
-constexpr int kTileVariants = 3;
+// 1 = finer split-K (>= 2 chunks per unit), 2 = coarser split-K (>= 8 chunks per unit), 3 = cluster
+// split-K (the default knobs on the cluster launch's co-resident grid, split counts rounded so the
+// splits of a tile are summed in distributed shared memory: csplit 4 or 2). Measured: the best
+// split-K granularity differs by network and stage (profiles/r1_kernel_ab_findings.md §5).
+constexpr int kTileVariants = 4;
+constexpr int kVariantCluster = 3;
+// the DSMEM group size of a split count (cluster split-K variant)
+int cluster_split_of(int split) { return split % 4 == 0 ? 4 : split % 2 == 0 ? 2 : 1; }
 void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms, int variant = 0) {
   TileKnobs kn = tile_knobs();
   if (variant == 1) kn.min_cps = std::max(1, kn.min_cps / 2);
   if (variant == 2) kn.min_cps = kn.min_cps * 2;
+  const bool csk = variant == kVariantCluster;
   const int target = kn.target_units > 0 ? kn.target_units : num_sms;
   for (GemmSpec* p : gs) {
     if (p->swap) {
@@ -581,6 +589,7 @@ void choose_tiling(std::vector<GemmSpec*>& gs, int simt_tiles, int num_sms, int 
       int want = std::min(best->split * 2, kn.max_split);
       const int room = (target - others) / (best->mt * best->ntn);
       if (kn.one_wave && want > room) want = room;
+      if (csk && want > 2) want = want >= 4 ? want / 4 * 4 : 2;   // splits a DSMEM group can sum
       if (want <= best->split || (best->kch + want - 1) / want < best_min_cps) break;
       best->cps = (best->kch + want - 1) / want;
       best->split = (best->kch + best->cps - 1) / best->cps;
@@ -718,12 +727,19 @@ void free_plan(DeviceState& d, StagePlan* p) {
 StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int variant = -1) {
   DeviceState& d = *g.dev;
   if (variant < 0) {
+    // untuned stages: the default knobs, or IOS_TILE_VARIANT (experiments / tests of one variant)
     auto vit = d.tile_variant.find(std::make_tuple(bpos, mask, strategy));
-    variant = vit == d.tile_variant.end() ? 0 : vit->second;
+    const char* ev = getenv("IOS_TILE_VARIANT");
+    const int dv = ev ? std::max(0, std::min(kTileVariants - 1, atoi(ev))) : 0;
+    variant = vit == d.tile_variant.end() ? dv : vit->second;
   }
   const std::vector<int> ops = g.ops_of(bpos, mask);
   PlanBuilder b(g);
   auto* plan = new StagePlan();
+  // cluster split-K variant: tiles sized for the cluster launch's co-resident grid (GPC sizes leave
+  // fewer SMs than the plain one-CTA-per-SM grid); no cluster support -> the default tiling
+  if (variant == kVariantCluster && (d.cluster_ctas <= 0 || g.math == IOS_MATH_FP32_SIMT)) variant = 0;
+  const int grid_sms = variant == kVariantCluster ? d.cluster_ctas : d.num_sms;
   try {
     if (strategy == IOS_MERGE) {
       // ---- operator merge (Z4): bounding-box kernel, stacked zero-padded filters,
@@ -892,7 +908,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       }
       // never more tiles than CTAs for one problem: a second wave doubles a latency-bound op
       if (p.kind != PK_GAVGPOOL)
-        p.items_per_tile = std::max(p.items_per_tile, (p.n_items + d.num_sms - 1) / d.num_sms);
+        p.items_per_tile = std::max(p.items_per_tile, (p.n_items + grid_sms - 1) / grid_sms);
       p.n_tiles = (p.n_items + p.items_per_tile - 1) / p.items_per_tile;
       simt_tiles += p.n_tiles;
     }
@@ -920,7 +936,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
         if (b.probs[i].kind == PK_GEMM) gs.push_back(&b.specs[i]);
         else ph_simt += b.probs[i].n_tiles;
       }
-      if (!gs.empty()) choose_tiling(gs, phased ? ph_simt : simt_tiles, d.num_sms, variant);
+      if (!gs.empty()) choose_tiling(gs, phased ? ph_simt : simt_tiles, grid_sms, variant);
     }
     size_t ws_bytes = 0;
     int n_tilectr = 0;
@@ -952,6 +968,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       p.split = s.split;
       p.chunks_per_split = s.cps;
       p.n_tiles = s.mt * s.ntn * s.split;
+      p.csplit = 1;
       if (p.split > 1) {
         p.workspace = ws_bytes;   // offset for now
         // one fp32 partial slab per split (<= kSlabSplits), else one zeroed reduction slab
@@ -962,11 +979,29 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
         n_tilectr += s.mt * s.ntn;
       }
     }
+    // ---- cluster split-K (variant 3): the csplit splits of an output tile are consecutive tiles
+    // starting at a multiple of csplit, so with a grid that is a multiple of the cluster size they
+    // run at the same time on consecutive ranks of one cluster (a halo-path stage keeps its fixed
+    // ring: no receive buffer; per-split slabs keep the deterministic global path)
+    bool csk_plan = false;
+    if (variant == kVariantCluster) {
+      bool halo = false;
+      for (Problem& p : b.probs) halo |= p.kind == PK_GEMM && p.hws != 0;
+      for (Problem& p : b.probs) {
+        if (p.kind != PK_GEMM || p.split < 2 || p.swap_ab || p.slabs || halo) continue;
+        p.csplit = cluster_split_of(p.split);
+        csk_plan |= p.csplit > 1;
+      }
+    }
+    for (Problem& p : b.probs)
+      if (p.kind != PK_GEMM) p.csplit = 1;
     // ---- tiles and counters: problems keep insertion (topological) order, so deps point back
     const int np = (int)b.probs.size();
     if (np > kMaxProblems) IOS_FAIL(IOS_ERR_UNSUPPORTED, "too many problems in one stage");
     int tiles = 0;
     for (Problem& p : b.probs) {
+      // padding tiles (skipped by every role) keep a csplit group on one cluster
+      if (csk_plan && p.csplit > 1) tiles = round_up(tiles, kClusterCtas);
       p.tile_begin = tiles;
       tiles += p.n_tiles;
     }
@@ -1141,27 +1176,42 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
         halo |= p.hws != 0;
       }
       static const int deep = getenv("IOS_DEEP_RING") ? atoi(getenv("IOS_DEEP_RING")) : 1;
+      // cluster split-K receive buffer at the end of the ring region: (csplit - 1) peers x the owned
+      // 128 / csplit rows x (BN fp32 + 16 B: conflict-free row-per-lane reads)
+      // (one row stride for the stage: the widest csplit problem's; the largest group form is
+      // csplit 4: 3 peers x 32 rows)
+      int rstride = 0;
+      for (Problem& p : b.probs)
+        if (p.kind == PK_GEMM && p.csplit > 1) rstride = std::max(rstride, p.BN * 4 + 16);
+      const int rbuf = rstride ? round_up((kBM - kBM / kClusterCtas) * rstride, 1024) : 0;
       if (halo || !deep) {
         sd.slot_bytes = kAStageBytes + kBStageBytes;
         sd.ring_slots = halo ? kStages - 1 : kStages;
       } else {
         sd.slot_bytes = kAStageBytes + round_up(max_bn * kChunkBytes, 1024);
-        sd.ring_slots = std::min(kMaxSlots, kRingBytes / sd.slot_bytes);
+        sd.ring_slots = std::min(kMaxSlots, (kRingBytes - rbuf) / sd.slot_bytes);
       }
+      if (rbuf && (halo || sd.ring_slots < 2)) IOS_FAIL(IOS_ERR_UNSUPPORTED, "cluster split-K receive buffer does not fit");
+      sd.cluster = csk_plan ? kClusterCtas : 1;
+      sd.rbuf_off = kRingBytes - rbuf;
+      sd.rbuf_stride = rstride;
+      if (csk_plan) sd.feat |= F_CSK;
       sd.has_gemm = 0;
       for (Problem& p : b.probs) sd.has_gemm |= p.kind == PK_GEMM;
       plan->grid = std::min(tiles, d.num_sms);
+      if (csk_plan) plan->grid = std::min(round_up(tiles, kClusterCtas), d.cluster_ctas);
       plan->dtype = g.dtype();
-      static const bool dump = getenv("IOS_DUMP_PLANS") && atoi(getenv("IOS_DUMP_PLANS")) != 0;
+      const bool dump = getenv("IOS_DUMP_PLANS") && atoi(getenv("IOS_DUMP_PLANS")) != 0;
       if (dump) {   // diagnostics: one line per problem of every plan built
-        fprintf(stderr, "[plan] block %d mask %llx T %d variant %d: %d tiles, grid %d, %d slots x %d B, feat %d\n", bpos,
-                (unsigned long long)mask, strategy, variant, tiles, plan->grid, sd.ring_slots, sd.slot_bytes, sd.feat);
+        fprintf(stderr, "[plan] block %d mask %llx T %d variant %d: %d tiles, grid %d, cluster %d, %d slots x %d B, feat %d\n",
+                bpos, (unsigned long long)mask, strategy, variant, tiles, plan->grid, sd.cluster, sd.ring_slots,
+                sd.slot_bytes, sd.feat);
         for (size_t i = 0; i < b.probs.size(); ++i) {
           const Problem& p = b.probs[i];
           if (p.kind == PK_GEMM)
-            fprintf(stderr, "[plan]   gemm M %d N %d K %d kch %d | BN %d ntn %d mt %d split %d cps %d | swap %d tma %d tt %d fdw %d deps %d\n",
+            fprintf(stderr, "[plan]   gemm M %d N %d K %d kch %d | BN %d ntn %d mt %d split %d cps %d csplit %d | swap %d tma %d tt %d fdw %d deps %d\n",
                     p.M, b.specs[i].N16, p.K, p.k_chunks, p.BN, p.n_tiles_n, p.m_tiles, p.split, p.chunks_per_split,
-                    p.swap_ab, p.a_tma, p.tt, p.fdw, p.n_deps);
+                    p.csplit, p.swap_ab, p.a_tma, p.tt, p.fdw, p.n_deps);
           else
             fprintf(stderr, "[plan]   simt kind %d tiles %d items %d deps %d\n", p.kind, p.n_tiles, p.n_items, p.n_deps);
         }
@@ -1256,7 +1306,12 @@ void tune_schedule(Graph& g, Schedule& q, int trials, int reps) {
     if (d.tile_variant.count(pk)) continue;   // tuned for an earlier schedule
     double best = kInf;
     int best_v = 0;
-    for (int v = 0; v < kTileVariants; ++v) {
+    // variants 0..2 by default; IOS_TUNE_VARIANTS=4 adds the cluster split-K variant (measured: the
+    // tuner then picks it for stages it wins in isolation, but the schedule gets slower in context --
+    // Inception V3 b=1 0.4915 -> 0.4967-0.5006 ms -- profiles/r2_cluster_split_k.md)
+    static const int nv = getenv("IOS_TUNE_VARIANTS") ? std::max(1, std::min(kTileVariants, atoi(getenv("IOS_TUNE_VARIANTS"))))
+                                                       : kVariantCluster;
+    for (int v = 0; v < nv; ++v) {
       StagePlan* p = nullptr;
       try {
         p = build_plan(g, bpos, mask, st.strategy, v);

@@ -123,6 +123,7 @@ void sync_and_check(Graph& g, cudaStream_t st);   // synchronise, then IOS_ERR_K
 
 // kernels (stage_kernel.cu)
 cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t st);
+int stage_cluster_ctas();   // co-resident CTAs of a cluster-split-K launch (clusters of kClusterCtas); 0 on error
 cudaError_t launch_nchw_to_nhwc(const float* in, const View& out, int dtype, int N, int C, cudaStream_t st);
 cudaError_t launch_nchw_unfold(const float* in, const View& out, int dtype, int N, int C, int W, int kw, int sw, int pw,
                                cudaStream_t st);

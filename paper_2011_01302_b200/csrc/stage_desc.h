@@ -140,6 +140,14 @@ struct Problem {
   uint64_t dwc;                     // fp32 chunk-major [k_chunks][k*k][elems per 128 B chunk] (halo path)
   int32_t hws, hhs;                 // halo path: input window of one patch tile = hhs rows x hws columns,
                                     // staged by ONE 4D tensor TMA (tmap_a) per K chunk, OOB = padding zeros
+  // cluster split-K (F_CSK): the split index s = g * csplit + r; the csplit splits of one output tile
+  // run on csplit CTAs of one thread-block cluster (tiles laid out so that r == cluster rank % csplit)
+  // and are summed through distributed shared memory: CTA rank r owns tile rows
+  // [r * 128 / csplit, (r + 1) * 128 / csplit); the others push their fp32 partial rows into its
+  // receive buffer (st.async + mbarrier complete_tx). With split == csplit that is the whole
+  // reduction; with more (split / csplit global groups) the owners' csplit-summed rows go through the
+  // global red.add + rendezvous path. 1 = no cluster reduction.
+  int32_t csplit, csk_pad_;
 };
 
 // Kernel feature classes: the stage kernel is instantiated per class with only the code paths its
@@ -149,8 +157,11 @@ enum KernelFeature : int32_t {
   F_GATHER = 1,   // implicit-im2col cp.async producer (pre-ReLU convs, narrow / unaligned inputs)
   F_FDW = 2,      // fused Relu-SepConv producers (halo + register forms)
   F_TRACE = 4,    // per-CTA %globaltimer timeline (ios_stage_trace)
+  F_CSK = 8,      // cluster split-K (Problem.csplit > 1): clusters of kClusterCtas CTAs, DSMEM reduction
 };
-constexpr int kFeatLean = 0, kFeatGather = F_GATHER, kFeatFull = F_GATHER | F_FDW, kFeatTrace = kFeatFull | F_TRACE;
+constexpr int kFeatLean = 0, kFeatGather = F_GATHER, kFeatFull = F_GATHER | F_FDW,
+              kFeatTrace = kFeatFull | F_TRACE | F_CSK;
+constexpr int kClusterCtas = 4;   // cluster size of F_CSK launches (csplit in {2, 4})
 
 // halo path (single-input fused Relu-SepConv): the stage runs its smem ring with 3 slots; slot 3's
 // B region holds the input window of the chunk, slot 3's A region the chunk's depthwise weights
@@ -178,6 +189,10 @@ struct StageDesc {
                                     // narrow tiles get a deeper ring (more bytes in flight per CTA)
   int32_t ring_slots;               // smem ring depth this launch (<= kMaxSlots), or 3 x 48 KB when a halo
                                     // problem borrows the last slot
+  int32_t cluster;                  // 1, or kClusterCtas: the launch is a cluster launch (F_CSK)
+  int32_t rbuf_off;                 // F_CSK: receive buffer at smem ring + rbuf_off (end of the ring region)
+  int32_t rbuf_stride;              // F_CSK: bytes per received row (the widest csplit problem's BN x 4 + 16)
+  int32_t pad_;
 };
 
 }  // namespace ios

@@ -49,6 +49,39 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t a, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
+// ---- cluster split-K (F_CSK): distributed shared memory between the CTAs of a cluster
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {   // own smem address -> peer's
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 16 B into a peer CTA's shared memory; the bytes complete_tx on the peer's mbarrier
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t rbar, uint32_t a, uint32_t b, uint32_t c,
+                                            uint32_t d) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%2, %3, %4, %5}, [%1];" ::"r"(raddr),
+               "r"(rbar), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t raddr) {   // release: prior reads of the buffer are done
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -1112,6 +1145,12 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   uint64_t* hbar = bars + 2 * kMaxSlots + 4;                // [2] halo + depthwise weights landed (halo path)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxSlots + 6);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+  // cluster split-K (F_CSK): rfull = this CTA's receive buffer holds every peer's partial rows;
+  // sempty[k] = the CTA of cluster rank k has consumed what this CTA last pushed to it
+  uint64_t* rfull = bars + 2 * kMaxSlots + 7;                 // [1]
+  uint64_t* sempty = bars + 2 * kMaxSlots + 8;                // [kClusterCtas]
+  constexpr bool kCsk = (FEAT & F_CSK) != 0;
+  const bool csk_launch = kCsk && sd.cluster > 1;
   float* sbias_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // 2 x kMaxBN
   uint8_t* sdesc = reinterpret_cast<uint8_t*>(bars) + kBarBytes + kBiasBytes;           // kDescBytes
   uint8_t* sepi = sdesc + kDescBytes;                                                     // kEpiBytes: 4 x 4 KB
@@ -1166,6 +1205,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     }
     mbar_init(smem_u32(&hbar[0]), 1);
     mbar_init(smem_u32(&hbar[1]), 1);
+    if (csk_launch) {
+      mbar_init(smem_u32(rfull), 1);
+      for (int k = 0; k < kClusterCtas; ++k) mbar_init(smem_u32(&sempty[k]), 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp && sd.has_gemm && DT != ET_F32X) {
@@ -1176,7 +1219,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  // a cluster launch: every peer's barriers are initialised before anyone pushes into them (this
+  // runs before the PDL wait, so it overlaps the previous stage's tail)
+  if (csk_launch) {
+    __syncwarp();
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Weight prefetch into L2: weights are never written by earlier stages, so
@@ -1261,6 +1311,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const Problem& P = probs[hint];
       if (P.kind != PK_GEMM) continue;
       const int local = t - P.tile_begin;
+      if (kCsk && local >= P.n_tiles) continue;   // cluster-alignment padding tile
       if (ptid == 0 && tfirst) IOS_TRACE(3);
       const TileCoord tc = tile_coord(P, local);
       const int mt = tc.mt, nt = tc.nt, c0 = tc.c0, c1 = tc.c1;
@@ -1554,6 +1605,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const Problem& P = probs[hint];
         if (P.kind != PK_GEMM) continue;
         const int local = t - P.tile_begin;
+        if (kCsk && local >= P.n_tiles) continue;   // cluster-alignment padding tile
         const int s = local - fdiv(P.fd_split, local) * P.split;
         const int c0 = s * P.chunks_per_split;
         const int c1 = min(c0 + P.chunks_per_split, P.k_chunks);
@@ -1596,10 +1648,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     const int lane_base = (warp & 3) * 32;        // TMEM lanes this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
+    // cluster split-K flow control (every epilogue warp keeps the same view): bit k of csk_sbits =
+    // parity of sempty[k]'s completed phases; csk_rphase = parity of rfull's
+    uint32_t csk_sbits = 0, csk_rphase = 0;
     int hint = 0;
     for (int t = blockIdx.x; t < sd.n_tiles; t += gridDim.x) {
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
+      if (kCsk && t - P.tile_begin >= P.n_tiles) continue;   // cluster-alignment padding tile
       if (P.kind != PK_GEMM) {
         if (warp == kEpilogueWarp0 && P.n_deps) {
 #ifdef IOS_ROW_BANDS
@@ -1870,7 +1926,72 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
       const int out_tile = mt * P.n_tiles_n + nt;
-      if (P.split == 1) {
+      // ---- cluster split-K: the csplit CTAs of this tile's group (consecutive cluster ranks) sum
+      // their partials in shared memory. Rank r owns rows [r * 128 / cD, (r + 1) * 128 / cD): those
+      // are the TMEM lanes of its epilogue warps q with q * cD / 4 == r. Every other warp pushes its
+      // 32 rows x BN fp32 into the owner's receive buffer (slot j = the sender's rank among the
+      // others), st.async completing bytes on the owner's rfull; the owner adds the cD - 1 received
+      // rows to its own before the store (or, with more splits than cD, before the global reduction).
+      int cD = 1;
+      bool c_owner = true;
+      uint32_t c_rbuf = 0;                   // this owner thread's row in receive slot 0
+      uint32_t c_rank = 0, c_gbase = 0;      // own cluster rank; cluster rank of the group's rank 0
+      int c_slot = 0;                        // bytes between receive slots
+      if constexpr (kCsk) {
+        if (P.csplit > 1) {
+          cD = P.csplit;
+          const int r = s % cD;
+          c_rank = cluster_rank();
+          c_gbase = c_rank - (uint32_t)r;
+          const int q = warp & 3, o = q * cD / 4;
+          const int rows_per = kBM / cD;
+          const int rr = (q - o * 4 / cD) * 32 + lane;     // row inside the owner's band
+          const uint32_t rbuf0 = smem_u32(smem + sd.rbuf_off);
+          c_slot = rows_per * sd.rbuf_stride;
+          c_owner = o == r;
+          if (!c_owner) {
+            const uint32_t oc = c_gbase + (uint32_t)o;
+            mbar_wait_cluster(smem_u32(&sempty[oc]), ((csk_sbits >> oc) & 1u) ^ 1u);
+            const int j = r < o ? r : r - 1;
+            const uint32_t rrow = mapa(rbuf0 + (uint32_t)(j * c_slot + rr * sd.rbuf_stride), oc);
+            const uint32_t rbar = mapa(smem_u32(rfull), oc);
+            for (int c0 = 0; c0 < BNx; c0 += 16) {
+              uint32_t v[16];
+              tmem_ld16(tbase + c0, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                st_async_v4(rrow + (uint32_t)(c0 + 4 * i) * 4u, rbar, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+          } else {
+            c_rbuf = rbuf0 + (uint32_t)(rr * sd.rbuf_stride);
+            if (lane == 0 && q == r * 4 / cD)
+              mbar_arrive_expect_tx(smem_u32(rfull), (uint32_t)((cD - 1) * rows_per * BNx * 4));
+          }
+          for (int k = 0; k < cD; ++k)
+            if (k != r) csk_sbits ^= 1u << (c_gbase + (uint32_t)k);
+          if (c_owner) mbar_wait_cluster(smem_u32(rfull), csk_rphase);
+          csk_rphase ^= 1u;
+        }
+      }
+      // owner: add the cD - 1 received partials of this thread's row, columns [c0, c0 + 32)
+      auto add_received = [&](int c0, float* o) {
+        if constexpr (kCsk) {
+          for (int j = 0; j < cD - 1; ++j) {
+            const uint32_t a = c_rbuf + (uint32_t)(j * c_slot + c0 * 4);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              uint32_t w0, w1, w2, w3;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(a + 16 * i));
+              o[4 * i] += __uint_as_float(w0);
+              o[4 * i + 1] += __uint_as_float(w1);
+              o[4 * i + 2] += __uint_as_float(w2);
+              o[4 * i + 3] += __uint_as_float(w3);
+            }
+          }
+        }
+      };
+      if (P.split == cD) {
         // Per 32-column round: TMEM -> registers (thread = row) -> bias/rounding -> this warp's 4 KB
         // smem staging tile (16 B pieces XOR-swizzled by row: conflict-free) -> coalesced 16 B global
         // stores (lanes sweep a row's contiguous channels; 4 rows per instruction) instead of 32
@@ -1886,7 +2007,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #pragma unroll
         for (int it = 0; it < 32 / RPI; ++it) opix[it] = pixel((warp & 3) * 32 + it * RPI + lane / PPR);
         const int sg0 = P.seg_begin, nsg = P.n_seg;
-        for (int c0 = 0; c0 < BNx; c0 += 32) {
+        for (int c0 = 0; c_owner && c0 < BNx; c0 += 32) {
           uint32_t va[16], vb[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
           acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
@@ -1894,7 +2015,10 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(13);
           float o[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(e < 16 ? va[e] : vb[e - 16]) + sbias[c0 + e];
+          for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(e < 16 ? va[e] : vb[e - 16]);
+          if (kCsk && cD > 1) add_received(c0, o);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] += sbias[c0 + e];
 #pragma unroll
           for (int p = 0; p < PPR; ++p) {
             uint32_t w[4];
@@ -1967,12 +2091,23 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // the splits of a tile reduce into the same lines: rotate the 32-column round and the 4-row
         // group order by split index so they do not queue on the same L2 lines at the same time
         const int nr32 = (BNx + 31) >> 5;
-        for (int k = 0; k < nr32; ++k) {
+        for (int k = 0; c_owner && k < nr32; ++k) {
           const int c0 = ((k + s) % nr32) * 32, rot = s;
           uint32_t va[16], vb[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
           acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
           acc_wait<DT>();
+          if (kCsk && cD > 1) {   // this owner's rows: the group's csplit partials summed first
+            float o[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(e < 16 ? va[e] : vb[e - 16]);
+            add_received(c0, o);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              va[e] = __float_as_uint(o[e]);
+              vb[e] = __float_as_uint(o[16 + e]);
+            }
+          }
           // stage (swizzled) then coalesced vector reductions: 4 rows x 128 B per instruction
 #pragma unroll
           for (int p = 0; p < 8; ++p) {
@@ -2076,11 +2211,19 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           }
         }
       }
-      if (P.signal) {
+      if (P.signal || cD > 1) {
         named_bar(2, 128);
         if (etid == 0) {
-          red_release_add(counters + P.done_idx, 1);
-          IOS_BAND_SIGNAL(mt);
+          if constexpr (kCsk) {
+            // this CTA's receive buffer is consumed: release it to every other rank of the group
+            const uint32_t mine = smem_u32(&sempty[c_rank]);
+            for (int k = 0; k < cD; ++k)
+              if (c_gbase + (uint32_t)k != c_rank) mbar_arrive_remote(mapa(mine, c_gbase + (uint32_t)k));
+          }
+          if (P.signal) {
+            red_release_add(counters + P.done_idx, 1);
+            IOS_BAND_SIGNAL(mt);
+          }
         }
       }
       tfirst = false;
@@ -2094,7 +2237,11 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   // ---------------------------------------------------------------------------- teardown
   __syncwarp();   // the MMA warp ran its loop on lane 0 only
   tc_fence_before();
-  __syncthreads();
+  // a cluster launch: no CTA leaves while a peer may still arrive on its barriers
+  if (csk_launch)
+    cluster_sync_all();
+  else
+    __syncthreads();
   if (warp == kMmaWarp && sd.has_gemm && DT != ET_F32X) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols) : "memory");
@@ -2113,7 +2260,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   cudaError_t launch_stage_inst_##dt##_##sdv##_##ft(cudaLaunchConfig_t& cfg, const StageDesc& sd)
 IOS_LAUNCHER_DEF3(IOS_INST_DT, IOS_INST_SD, IOS_INST_FEAT) {
   static bool attr_done = false;
-  static int max_grid = 0;
+  static int max_grid = 0, max_cluster_grid = 0;
   auto k = ios_stage_kernel<IOS_INST_DT, (IOS_INST_SD != 0), IOS_INST_FEAT>;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024);
@@ -2125,11 +2272,51 @@ IOS_LAUNCHER_DEF3(IOS_INST_DT, IOS_INST_SD, IOS_INST_FEAT) {
     if (e != cudaSuccess) return e;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     max_grid = per_sm * sms;
+    if ((IOS_INST_FEAT & F_CSK) != 0) {
+      // clusters of kClusterCtas one-CTA-per-SM blocks fit fewer SMs than the plain grid (GPC sizes)
+      cudaLaunchConfig_t q = cfg;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = kClusterCtas;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      q.attrs = a;
+      q.numAttrs = 1;
+      q.gridDim = dim3(kClusterCtas * 8);
+      int nc = 0;
+      e = cudaOccupancyMaxActiveClusters(&nc, (const void*)k, &q);
+      if (e != cudaSuccess) return e;
+      max_cluster_grid = nc * kClusterCtas;
+    }
     attr_done = true;
   }
-  if ((int)(cfg.gridDim.x) > max_grid) return cudaErrorCooperativeLaunchTooLarge;
+  bool cluster = false;
+  for (unsigned i = 0; i < cfg.numAttrs; ++i) cluster |= cfg.attrs[i].id == cudaLaunchAttributeClusterDimension;
+  if ((int)(cfg.gridDim.x) > (cluster ? max_cluster_grid : max_grid)) return cudaErrorCooperativeLaunchTooLarge;
   return cudaLaunchKernelEx(&cfg, k, sd);
 }
+#if IOS_INST_DT == 0 && IOS_INST_SD == 1 && IOS_INST_FEAT == 8   // (F_CSK: an enum, not visible to #if)
+// co-resident CTAs of a cluster launch (clusters of kClusterCtas, one CTA per SM); 0 on error
+int stage_cluster_ctas() {
+  auto k = ios_stage_kernel<0, true, F_CSK>;
+  if (cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes + 1024) != cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t q{};
+  q.gridDim = dim3(kClusterCtas * 8);
+  q.blockDim = dim3(kThreads);
+  q.dynamicSmemBytes = kSmemBytes + 1024;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = kClusterCtas;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  q.attrs = a;
+  q.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, (const void*)k, &q) != cudaSuccess) return 0;
+  return nc * kClusterCtas;
+}
+#endif
 
 }  // namespace ios
 #else
@@ -2196,17 +2383,18 @@ __global__ void l2_flush_kernel(int4* buf, int64_t n) {
 #define IOS_LAUNCHER_DECL(dt, sdv, ft) \
   cudaError_t launch_stage_inst_##dt##_##sdv##_##ft(cudaLaunchConfig_t& cfg, const StageDesc& sd)
 #define IOS_DECL_CLASSES(dt, sdv) \
-  IOS_LAUNCHER_DECL(dt, sdv, 0); IOS_LAUNCHER_DECL(dt, sdv, 1); IOS_LAUNCHER_DECL(dt, sdv, 3); IOS_LAUNCHER_DECL(dt, sdv, 7)
+  IOS_LAUNCHER_DECL(dt, sdv, 0); IOS_LAUNCHER_DECL(dt, sdv, 1); IOS_LAUNCHER_DECL(dt, sdv, 3); \
+  IOS_LAUNCHER_DECL(dt, sdv, 8); IOS_LAUNCHER_DECL(dt, sdv, 9); IOS_LAUNCHER_DECL(dt, sdv, 11); IOS_LAUNCHER_DECL(dt, sdv, 15)
 IOS_DECL_CLASSES(0, 0); IOS_DECL_CLASSES(0, 1); IOS_DECL_CLASSES(1, 0); IOS_DECL_CLASSES(1, 1);
-IOS_LAUNCHER_DECL(2, 0, 3); IOS_LAUNCHER_DECL(2, 1, 3); IOS_LAUNCHER_DECL(2, 0, 7); IOS_LAUNCHER_DECL(2, 1, 7);
+IOS_LAUNCHER_DECL(2, 0, 3); IOS_LAUNCHER_DECL(2, 1, 3); IOS_LAUNCHER_DECL(2, 0, 15); IOS_LAUNCHER_DECL(2, 1, 15);
 
 namespace {
 // smallest compiled class covering the stage's features (FP32-SIMT: the full class only)
 int feature_class(int dtype, int feat) {
   if (feat & F_TRACE) return kFeatTrace;
-  if (dtype == ET_F32X || (feat & F_FDW)) return kFeatFull;
-  if (feat & F_GATHER) return kFeatGather;
-  return kFeatLean;
+  int c = (dtype == ET_F32X || (feat & F_FDW)) ? kFeatFull : (feat & F_GATHER) ? kFeatGather : kFeatLean;
+  if ((feat & F_CSK) && dtype != ET_F32X) c |= F_CSK;
+  return c;
 }
 }  // namespace
 
@@ -2216,7 +2404,7 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes + 1024;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
@@ -2229,15 +2417,24 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
     attr[1].val.cooperative = 1;
     cfg.numAttrs = 2;
   }
+  // cluster split-K stages launch as clusters of kClusterCtas (grid a multiple of it)
+  if (sd.cluster > 1) {
+    attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    attr[cfg.numAttrs].val.clusterDim.x = (unsigned)sd.cluster;
+    attr[cfg.numAttrs].val.clusterDim.y = 1;
+    attr[cfg.numAttrs].val.clusterDim.z = 1;
+    ++cfg.numAttrs;
+  }
   const int sdv = sd.blob_bytes <= kDescBytes ? 1 : 0;
   const int fc = feature_class(dtype, sd.feat | (sd.trace ? F_TRACE : 0));
 #define IOS_DISPATCH(dt, sv, f) \
   if (dtype == dt && sdv == sv && fc == f) return launch_stage_inst_##dt##_##sv##_##f(cfg, sd)
-  IOS_DISPATCH(0, 1, 0); IOS_DISPATCH(0, 1, 1); IOS_DISPATCH(0, 1, 3); IOS_DISPATCH(0, 1, 7);
-  IOS_DISPATCH(0, 0, 0); IOS_DISPATCH(0, 0, 1); IOS_DISPATCH(0, 0, 3); IOS_DISPATCH(0, 0, 7);
-  IOS_DISPATCH(1, 1, 0); IOS_DISPATCH(1, 1, 1); IOS_DISPATCH(1, 1, 3); IOS_DISPATCH(1, 1, 7);
-  IOS_DISPATCH(1, 0, 0); IOS_DISPATCH(1, 0, 1); IOS_DISPATCH(1, 0, 3); IOS_DISPATCH(1, 0, 7);
-  IOS_DISPATCH(2, 1, 3); IOS_DISPATCH(2, 1, 7); IOS_DISPATCH(2, 0, 3); IOS_DISPATCH(2, 0, 7);
+#define IOS_DISPATCH_ALL(dt, sv) \
+  IOS_DISPATCH(dt, sv, 0); IOS_DISPATCH(dt, sv, 1); IOS_DISPATCH(dt, sv, 3); IOS_DISPATCH(dt, sv, 8); \
+  IOS_DISPATCH(dt, sv, 9); IOS_DISPATCH(dt, sv, 11); IOS_DISPATCH(dt, sv, 15)
+  IOS_DISPATCH_ALL(0, 1); IOS_DISPATCH_ALL(0, 0); IOS_DISPATCH_ALL(1, 1); IOS_DISPATCH_ALL(1, 0);
+  IOS_DISPATCH(2, 1, 3); IOS_DISPATCH(2, 1, 15); IOS_DISPATCH(2, 0, 3); IOS_DISPATCH(2, 0, 15);
+#undef IOS_DISPATCH_ALL
 #undef IOS_DISPATCH
   return cudaErrorInvalidValue;
 }

@@ -200,3 +200,26 @@ def test_refined_schedule_valid_and_parity(torch_cuda, name, math):
     assert q.stats[3] // 1000 >= 1                       # at least the plain DP's candidate
     assert sorted(v for ops, _, _ in q.stages for v in ops) == list(range(1, net.n_ops + 1))
     _check_run(net, math, g, q, torch_cuda)
+
+
+@pytest.mark.parametrize("name,math,batch", [("inception_v3", "tf32", 1), ("squeezenet", "tf32", 1),
+                                             ("randwire_ws_small", "bf16", 1), ("nasnet_a_large", "tf32", 1),
+                                             ("inception_v3", "tf32", 8)])
+def test_cluster_split_k_variant(torch_cuda, monkeypatch, capfd, name, math, batch):
+    """Tiling variant 3 (cluster split-K: the csplit splits of an output tile summed in distributed
+    shared memory of a 4-CTA cluster, csplit 2 and 4, with and without a further global split-K
+    level) forced on every stage: the fewest-stages schedule (chains + groups) and greedy, per op and
+    end to end. The plan dump proves cluster launches with both group sizes ran."""
+    from paper_2011_01302_b200 import Graph
+    monkeypatch.setenv("IOS_TILE_VARIANT", "3")
+    monkeypatch.setenv("IOS_DUMP_PLANS", "1")
+    net = W.build(name, math=math, batch=batch)
+    g = Graph.from_netspec(net, math)
+    q = g.schedule_dp(3, 8, lambda b, m, t: 1.0 + (0.5 if t == 1 else 0.0))
+    _check_run(net, math, g, q, torch_cuda)
+    _check_run(net, math, g, g.schedule_greedy(), torch_cuda, ops=[])
+    dump = capfd.readouterr().err
+    if name in ("inception_v3", "squeezenet"):   # (RandWire / NASNet b=1: swap-AB tiles, no split groups)
+        assert "cluster 4" in dump
+    if name == "inception_v3":
+        assert "csplit 4" in dump and "csplit 2" in dump

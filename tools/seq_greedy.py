@@ -17,15 +17,19 @@ from paper_2011_01302_b200 import Graph  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--net", default="nasnet_a_large")
 ap.add_argument("--steps", type=int, default=30)
+ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--tune", type=int, default=0, help="1: stage-tune both schedules first (ios_schedule_tune)")
 a = ap.parse_args()
 math = NETS[a.net]["math"]
-net = W.build(a.net, math=math)
+net = W.build(a.net, math=math, batch=a.batch)
 g = Graph.from_netspec(net, math)
 x = torch.from_numpy(net.make_input()).cuda()
 out = torch.empty(g.output_shape(), dtype=torch.float32, device="cuda")
 flush = torch.empty(int(2 * torch.cuda.get_device_properties(0).L2_cache_size) // 4 + 1024, device="cuda")
 res = {}
 for name, q in (("sequential", g.schedule_sequential()), ("greedy", g.schedule_greedy())):
+    if a.tune:
+        g.tune(q)
     for _ in range(3):
         g.run(q, x, out)
     torch.cuda.synchronize()

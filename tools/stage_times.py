@@ -20,12 +20,13 @@ from paper_2011_01302_b200 import Graph  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--schedule", required=True)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--variants", type=int, default=1, help="0: ignore the saved tile variants (IOS_TILE_VARIANT applies)")
 a = ap.parse_args()
 sj = json.load(open(a.schedule))
 net = W.build(sj["net"], math=sj["math"], batch=sj["batch"])
 g = Graph.from_netspec(net, sj["math"])
 q = g.schedule([(ops, t) for ops, t in sj["stages"]])
-if os.path.exists(a.schedule + ".variants"):
+if a.variants and os.path.exists(a.schedule + ".variants"):
     g.load_tile_variants(a.schedule + ".variants")
 x = torch.from_numpy(net.make_input()).cuda()
 out = torch.empty(g.output_shape(), dtype=torch.float32, device="cuda")
