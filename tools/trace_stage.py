@@ -17,6 +17,9 @@ for ops, t in stages:
     a = np.array(buf[:grid.value * 16], dtype=np.int64).reshape(grid.value, 16)[:, :16]
     # slot 0: globaltimer ns at CTA entry; slots 1-15: SM cycles since entry + 1 (ios.h)
     ghz = float(os.environ.get("IOS_SM_GHZ", "1.965"))
+    if not (a[:, 0] > 0).any():
+        print(f"stage {ops} T={t}: no trace stamps (grid {grid.value})")
+        continue
     t0 = a[:, 0][a[:, 0] > 0].min()
     ent = (a[:, :1] - t0) / 1000.0
     rel = np.where(a > 0, ent + (a - 1) / (ghz * 1000.0), np.nan)
@@ -24,6 +27,8 @@ for ops, t in stages:
     print(f"stage {ops} T={t} profiled {ms*1e3:.1f} us, grid {grid.value}; us since first entry (min/median/max over CTAs):")
     names = ["entry", "prologue", "P 1st issued", "P tile start", "mma done", "acc1 ready", "epi done", "teardown", "exit",
              "P expect_tx", "P A issued", "own prologue", "P 2nd issued", "e:13", "e:14", "e:15"]
+    if os.environ.get("IOS_TRACE_FINE_NAMES"):   # libios built with -DIOS_TRACE_FINE
+        names[13:16] = ["PDL wait done", "P tile decoded", "P TMA geom"]
     for k, nm in enumerate(names):
         col = rel[:, k]
         col = col[~np.isnan(col)]
