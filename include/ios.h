@@ -159,10 +159,12 @@ IOS_API ios_status ios_schedule_dp_ex(ios_graph g, int32_t r, int32_t s, ios_str
                               void* ctx, ios_schedule* out, double* out_cost_ms, int64_t out_stats[3]);
 /* Measured refinement (an engine extension beyond the paper): the device-profiled DP is run under a
  * small family of cost models -- pruning (r, s), (min(r,2), s), (1, s), each with every measured
- * stage latency biased by -beta_us, 0, +beta_us -- every distinct candidate schedule is stage-tuned
- * and run in context (ios_run_timeline, `reps` runs, L2 flushed), and each block keeps the
- * candidate whose stages took the least in-run time there. Every stage of the result is a stage
- * some DP optimum chose. out_stats (may be NULL): [0..2] as ios_schedule_dp_ex for (r, s) unbiased,
+ * stage latency biased by -beta_us, 0, +beta_us -- plus the greedy and sequential stages of every
+ * block whose greedy stages lie in P(r, s) (other blocks keep the plain DP's stages); every
+ * distinct candidate schedule is stage-tuned and run in context (ios_run_timeline, `reps` runs, L2
+ * flushed), and each block keeps the candidate whose stages took the least in-run time there.
+ * Every block of the result is a schedule in Algorithm 1's search space under pruning (r, s),
+ * chosen by measurement. out_stats (may be NULL): [0..2] as ios_schedule_dp_ex for (r, s) unbiased,
  * [3] = candidates * 1000 + blocks taken from a candidate other than the plain DP. Synchronises. */
 IOS_API ios_status ios_schedule_refine(ios_graph g, int32_t r, int32_t s, int32_t reps, double beta_us,
                                        ios_schedule* out, int64_t out_stats[4]);

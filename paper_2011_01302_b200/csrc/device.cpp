@@ -893,8 +893,12 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       const bool win = sq && ((p.kind == PK_DWCONV && (p.kh == 3 || p.kh == 5 || p.kh == 7) && p.n_in <= 8) ||
                               ((p.kind == PK_MAXPOOL || p.kind == PK_AVGPOOL) && p.kh == 3));
       if (p.kind == PK_GAVGPOOL) {
+        // 4 items per warp that runs SIMT tiles: the 4 epilogue warps, or all 9 warps of a stage
+        // without GEMM members (more loads in flight per SM at large batch)
+        bool any_gemm = false;
+        for (const Problem& q : b.probs) any_gemm |= q.kind == PK_GEMM;
         p.n_items = p.batch * nvec;
-        p.items_per_tile = 16;
+        p.items_per_tile = any_gemm ? 16 : 4 * (kThreads / 32);
       } else if (win) {
         // quads of horizontally adjacent outputs (win_tile in stage_kernel.cu); one quad x vector
         // per thread of a 128-thread tile
@@ -974,7 +978,8 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
         // one fp32 partial slab per split (<= kSlabSplits), else one zeroed reduction slab
         static const int slab_splits = getenv("IOS_SLAB_SPLITS") ? atoi(getenv("IOS_SLAB_SPLITS")) : kSlabSplits;
         p.slabs = s.split <= slab_splits ? 1 : 0;
-        ws_bytes += (size_t)s.mt * s.ntn * (p.slabs ? s.split : 1) * kBM * s.BN * sizeof(float);
+        const size_t copies = p.slabs ? s.split : 1;
+        ws_bytes += (size_t)s.mt * s.ntn * copies * kBM * s.BN * sizeof(float);
         p.tilectr_idx = n_tilectr;
         n_tilectr += s.mt * s.ntn;
       }

@@ -242,6 +242,53 @@ void schedule_refine(Graph& g, int r, int s, int reps, double beta_ms, Schedule*
       keys.push_back(k);
       cands.push_back(std::move(q));
     }
+  // + the baseline schedules where they lie in the search space: per block, the greedy stages when
+  // every one satisfies P(r, s) (greedy groups are single ops: at most s ready ops), and the
+  // sequential stages (always in P). Blocks outside P keep the plain DP's stages, so every block of
+  // the result is still a schedule of Algorithm 1's search space, picked by in-context measurement.
+  {
+    const int nb0 = (int)g.blocks.size();
+    Schedule qg, qs;
+    qg.g = qs.g = &g;
+    for (int bp = 0; bp < nb0; ++bp) {
+      const BlockInfo& b = g.blocks[bp];
+      const int n = (int)b.ops.size();
+      const uint64_t all = n == 64 ? ~0ull : ((1ull << n) - 1);
+      std::vector<Stage> gst;
+      bool in_p = true;
+      for (uint64_t rem = all; rem;) {
+        uint64_t ready = 0;
+        for (int i = 0; i < n; ++i)
+          if ((rem >> i & 1) && !(b.pred[i] & rem)) ready |= 1ull << i;
+        if (s > 0 && popcount64(ready) > s) in_p = false;
+        Stage st;
+        st.ops = g.ops_of(bp, ready);
+        gst.push_back(st);
+        rem &= ~ready;
+      }
+      if (!in_p) {
+        gst.clear();
+        for (const Stage& x : cands[0].stages) {
+          int bpos = -1;
+          g.mask_of(x.ops, &bpos);
+          if (bpos == bp) gst.push_back(x);
+        }
+      }
+      for (Stage& x : gst) qg.stages.push_back(x);
+      for (int i = 0; i < n; ++i) {
+        Stage st;
+        st.ops = {b.ops[i]};
+        qs.stages.push_back(st);
+      }
+    }
+    for (Schedule* q : {&qg, &qs}) {
+      std::vector<std::pair<std::vector<int>, int>> k;
+      for (const Stage& x : q->stages) k.push_back({x.ops, x.strategy});
+      if (std::find(keys.begin(), keys.end(), k) != keys.end()) continue;
+      keys.push_back(k);
+      cands.push_back(std::move(*q));
+    }
+  }
   // per-block in-run time of every candidate
   const int nb = (int)g.blocks.size();
   std::vector<std::vector<double>> block_us(cands.size(), std::vector<double>(nb, 0.0));

@@ -921,9 +921,10 @@ __device__ __noinline__ void simt_tile(const Problem& P, const View* views, int 
     return;
   }
   if (P.kind == PK_GAVGPOOL) {
-    // 16 (image, channel vector) items per tile on warps 0-3: lane = (pixel phase p, item il);
-    // 8 pixel phases per item, 4 loads in flight per lane, shuffle-reduced over the phases
-    if (tid >= 128) return;
+    // 4 (image, channel vector) items per warp (items_per_tile / 4 warps: 4 on epilogue warps,
+    // 9 when the stage runs SIMT on every warp): lane = (pixel phase p, item il); 8 pixel phases
+    // per item, 8 loads in flight per lane, shuffle-reduced over the phases
+    if (tid >= P.items_per_tile * 8) return;
     const View& in = views[P.in_begin];
     const int hw = in.H * in.W;
     const float inv = 1.0f / (float)hw;
@@ -934,13 +935,13 @@ __device__ __noinline__ void simt_tile(const Problem& P, const View* views, int 
     const int n = ok ? idx / nvec : 0, v = ok ? idx - (idx / nvec) * nvec : 0;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (ok) {
-      for (int p0 = p; p0 < hw; p0 += 32) {
-        float x[4][8];
+      for (int p0 = p; p0 < hw; p0 += 64) {
+        float x[8][8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 8; ++u)
           if (p0 + 8 * u < hw) ld16<DT>(in, (int64_t)n * hw + p0 + 8 * u, v * NV, x[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 8; ++u)
           if (p0 + 8 * u < hw) {
 #pragma unroll
             for (int e = 0; e < NV; ++e) acc[e] += relu ? fmaxf(x[u][e], 0.f) : x[u][e];
@@ -1186,6 +1187,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) IOS_TRACE(0);
+  // Launch epoch: every CTA of a launch adds 1 to the plan's 64-bit launch counter (counters[0..1])
+  // exactly once, before the launch triggers its dependents (launch_dependents below), so old / grid
+  // is this launch's number for every CTA (it never wraps; the epoch itself is used mod 2^32). Every
+  // CTA of an earlier launch of this plan added its 1 before that launch triggered ITS dependents,
+  // so the value is final whenever this grid runs: the add is issued first thing, its L2 round trip
+  // overlapping the descriptor copy and the barrier / TMEM set-up; the prologue barrier publishes it.
+  unsigned long long ep_old = 0;
+  if (sd.uses_counters && tid == 0) ep_old = atomicAdd(reinterpret_cast<unsigned long long*>(counters), 1ull);
 
   if (desc_in_smem) {
     const int4* src = reinterpret_cast<const int4*>(sd.problems);
@@ -1210,6 +1219,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       for (int k = 0; k < kClusterCtas; ++k) mbar_init(smem_u32(&sempty[k]), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (sd.uses_counters) *flag = (int)(uint32_t)(ep_old / gridDim.x);
   }
   if (warp == kMmaWarp && sd.has_gemm && DT != ET_F32X) {
     __syncwarp();
@@ -1240,30 +1250,34 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #ifndef IOS_NO_TMAP_PREFETCH
       if (P.tmap_a) prefetch_tmap(P.tmap_a);   // descriptor fetch off the first TMA's critical path
 #endif
-      const uint64_t total = (uint64_t)P.k_chunks * P.Npad8 * kChunkBytes;
-      const uint64_t share = ((total + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
-      const uint64_t b0 = share * blockIdx.x, b1 = b0 + share < total ? b0 + share : total;
-      for (uint64_t o = b0; o < b1; o += 32768)
-        prefetch_l2(reinterpret_cast<const uint8_t*>(P.wts) + o, (uint32_t)(b1 - o < 32768 ? b1 - o : 32768));
+      // (32-bit: packed weights of one GEMM are < 4 GB; a 64-bit division is a ~100-instruction call)
+      const uint32_t total = (uint32_t)P.k_chunks * (uint32_t)P.Npad8 * kChunkBytes;
+      const uint32_t share = ((total + gridDim.x - 1) / gridDim.x + 15) & ~15u;
+      const uint32_t b0 = share * blockIdx.x, b1 = b0 + share < total ? b0 + share : total;
+      for (uint32_t o = b0; o < b1; o += 32768)
+        prefetch_l2(reinterpret_cast<const uint8_t*>(P.wts) + o, b1 - o < 32768 ? b1 - o : 32768);
     }
   }
 #endif
-  // launch epoch: every CTA of a launch adds 1 to the launch counter exactly once, before releasing the
-  // next launch (launch_dependents), so old / grid is this launch's number for every CTA
-  // (64-bit, in counters[0..1]: it never wraps; the epoch itself is used mod 2^32). The counters are
-  // the plan's own, and every CTA of an earlier launch of this plan added its 1 before that launch
-  // triggered its dependents, so the add is issued BEFORE the PDL wait: its L2 round trip overlaps
-  // the previous grid's tail instead of delaying every role after the wait.
-  unsigned long long ep_old = 0;
-  if (sd.uses_counters && tid == 0) ep_old = atomicAdd(reinterpret_cast<unsigned long long*>(counters), 1ull);
-  // programmatic dependent launch: the prologue above overlapped the previous stage's tail; from
-  // here on we read activations (and counters) the previous grid may still be writing
-  if (tid == 0) IOS_TRACE(11);   // before waiting for the previous grid
-  pdl_wait();
-  if (sd.stamp && tid == 0) atomicMin(reinterpret_cast<unsigned long long*>(sd.stamp), (unsigned long long)gtimer());
-  if (sd.uses_counters && tid == 0) *flag = (int)(uint32_t)(ep_old / gridDim.x);
-  pdl_launch_dependents();
-  named_bar(4, kThreads);
+  // Late PDL wait: no CTA-wide wait here. Each thread executes griddepcontrol.wait right before its
+  // first access to data an earlier grid writes (activations; the split-K workspace): producers
+  // after decoding their first tile (and its in-stage dependency wait: counters are this plan's own,
+  // epoch-relative and monotonic, so they are safe to poll early), epilogue / SIMT threads before
+  // their first tile's loads or stores; the MMA warp never touches global memory. Tile decode and
+  // the code those paths first execute then overlap the previous stage's tail.
+  bool pdl_done = false;
+  auto lazy_pdl = [&]() {
+    if (!pdl_done) {
+      pdl_wait();
+      pdl_done = true;
+#ifdef IOS_TRACE_FINE
+      if (tid == 0) IOS_TRACE(13);   // PDL wait returned
+#endif
+      if (sd.stamp && tid == 0) atomicMin(reinterpret_cast<unsigned long long*>(sd.stamp), (unsigned long long)gtimer());
+    }
+  };
+  if (tid == 0) IOS_TRACE(11);
+  pdl_launch_dependents();   // every CTA's epoch add is done (published by the prologue barrier)
   const uint32_t ep = sd.uses_counters ? (uint32_t)*flag : 0u;
   if (tid == 0) IOS_TRACE(1);
 
@@ -1273,6 +1287,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
     for (int t = blockIdx.x; t < sd.n_tiles; t += gridDim.x) {
       hint = find_problem(sm_tile_begin, sd.n_problems, t, hint);
       const Problem& P = probs[hint];
+      lazy_pdl();
       if (warp == 0 && P.n_deps) {
 #ifdef IOS_ROW_BANDS
         int g0, g1;
@@ -1314,6 +1329,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       if (kCsk && local >= P.n_tiles) continue;   // cluster-alignment padding tile
       if (ptid == 0 && tfirst) IOS_TRACE(3);
       const TileCoord tc = tile_coord(P, local);
+#ifdef IOS_TRACE_FINE
+      if (ptid == 0 && tfirst) IOS_TRACE(14);   // tile decoded
+#endif
       const int mt = tc.mt, nt = tc.nt, c0 = tc.c0, c1 = tc.c1;
       if (P.n_deps) {
         if (warp == 0) {
@@ -1327,6 +1345,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         }
         named_bar(1, 128);
       }
+      lazy_pdl();
       if constexpr ((FEAT & F_FDW) != 0 && DT != ET_F32X) if (P.fdw) {
         // fused Relu-SepConv: depthwise computed into the A slot, pointwise weights by bulk copy
         const int rr = fdiv(P.fd_tilw, mt);
@@ -1427,6 +1446,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             iw0 = tw * P.tWt * P.sw - P.pw;
             xbytes = (uint32_t)(P.tN * P.tR * P.tWt) * kChunkBytes;
           }
+#ifdef IOS_TRACE_FINE
+          if (lane == 0 && tfirst) IOS_TRACE(15);   // TMA geometry ready
+#endif
           for (int c = c0; c < c1; ++c) {
             mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
             if (lane == 0) {
@@ -1657,6 +1679,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       const Problem& P = probs[hint];
       if (kCsk && t - P.tile_begin >= P.n_tiles) continue;   // cluster-alignment padding tile
       if (P.kind != PK_GEMM) {
+        lazy_pdl();
         if (warp == kEpilogueWarp0 && P.n_deps) {
 #ifdef IOS_ROW_BANDS
           int g0, g1;
@@ -1763,6 +1786,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           __syncwarp();
         };
         mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+        lazy_pdl();
         if (etid == 0 && tfirst) IOS_TRACE(5);
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
@@ -1922,6 +1946,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
       for (int i = etid; i < BNx; i += 128) sbias[i] = __ldg(bias + nt * BNx + i);
       named_bar(2, 128);
       if (DT != ET_F32X) mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+      lazy_pdl();
       if (etid == 0 && tfirst) IOS_TRACE(5);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
@@ -2012,7 +2037,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
           acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
           acc_wait<DT>();
+#ifndef IOS_TRACE_FINE
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(13);
+#endif
           float o[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(e < 16 ? va[e] : vb[e - 16]);
@@ -2036,7 +2063,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
                          "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
           }
           __syncwarp();
+#ifndef IOS_TRACE_FINE
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(14);
+#endif
           // this lane's piece column and its segment (destination, channel stride, ReLU)
           const int p = lane % PPR;
           const int ncol = nt * BNx + c0 + p * (16 / OESZ);
@@ -2073,7 +2102,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             if (opix[it] >= 0 && dst) stg_v4(dst + (int64_t)opix[it] * ocs * OESZ, w[0], w[1], w[2], w[3]);
           }
           __syncwarp();
+#ifndef IOS_TRACE_FINE
           if (etid == 0 && tfirst && c0 == 0) IOS_TRACE(15);
+#endif
         }
         tc_fence_before();
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
@@ -2135,10 +2166,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         tc_fence_before();
         if (DT != ET_F32X) mbar_arrive(smem_u32(&tempty[acc]));
         named_bar(2, 128);
+#ifndef IOS_TRACE_FINE
         if (etid == 0 && tfirst) IOS_TRACE(13);
+#endif
         if (warp == kEpilogueWarp0) split_rendezvous(counters + P.tilectr_idx + out_tile, P.split, err, ep, lane);
         named_bar(2, 128);
+#ifndef IOS_TRACE_FINE
         if (etid == 0 && tfirst) IOS_TRACE(14);
+#endif
         {
           // distributed finalize (see the swap-AB path): split s owns tile rows
           // [s*trows/S, (s+1)*trows/S); all 128 threads, coalesced (consecutive threads sweep a
@@ -2321,52 +2356,79 @@ int stage_cluster_ctas() {
 }  // namespace ios
 #else
 // ------------------------------------------------------------------------ boundary layout kernels
+// 8 consecutive channels of one pixel as 16 B vector stores (32 B fp32 / 16 B bf16; C is padded to a
+// multiple of 8, views are 16 B aligned: layout_ok)
+__device__ __forceinline__ void store8(const View& vw, int dtype, int64_t pix, int c0, const float* v) {
+  if (dtype != ET_BF16) {
+    float* d = reinterpret_cast<float*>(vw.ptr) + pix * vw.cstride + vw.coff + c0;
+    stg_v4(d, __float_as_uint(rnd(v[0], dtype)), __float_as_uint(rnd(v[1], dtype)), __float_as_uint(rnd(v[2], dtype)),
+           __float_as_uint(rnd(v[3], dtype)));
+    stg_v4(d + 4, __float_as_uint(rnd(v[4], dtype)), __float_as_uint(rnd(v[5], dtype)), __float_as_uint(rnd(v[6], dtype)),
+           __float_as_uint(rnd(v[7], dtype)));
+  } else {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = (uint32_t)bf16_bits(v[2 * q]) | ((uint32_t)bf16_bits(v[2 * q + 1]) << 16);
+    stg_v4(reinterpret_cast<__nv_bfloat16*>(vw.ptr) + pix * vw.cstride + vw.coff + c0, w[0], w[1], w[2], w[3]);
+  }
+}
+
 // NCHW fp32 (caller) -> NHWC padded (internal); rounds to the storage precision (Z14).
+// Thread = (8-channel group g, pixel), pixel fastest: a warp reads 32 consecutive pixels of each of
+// its 8 planes (coalesced) and writes 32 full 32 B sectors.
 __global__ void nchw_to_nhwc_kernel(const float* __restrict__ in, View out, int dtype, int N, int C) {
-  const int64_t total = (int64_t)N * out.H * out.W * out.C;
-  const int64_t hw = (int64_t)out.H * out.W;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % out.C);
-    const int64_t pix = i / out.C;
-    const int64_t n = pix / hw, p = pix % hw;
-    const float x = c < C ? in[(n * C + c) * hw + p] : 0.f;
-    store_elem(out, dtype, pix, c, x);
+  const int hw = out.H * out.W;
+  const int npix = N * hw, ng = out.C / 8;
+  const int total = npix * ng;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i / npix, pix = i - g * npix;
+    const int n = pix / hw, p = pix - n * hw;
+    const float* src = in + (int64_t)n * C * hw + p;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = 8 * g + e < C ? __ldg(src + (int64_t)(8 * g + e) * hw) : 0.f;
+    store8(out, dtype, pix, 8 * g, v);
   }
 }
 
 // NCHW fp32 (caller) -> the W-unfolded NHWC input of a narrow first conv (DeviceState::unfold):
 // out pixel (n, h, ow), channel j * C + c = in[n, c, h, ow*sw - pw + j] (0 outside the image and in
-// the padding channels), rounded to the storage precision.
+// the padding channels), rounded to the storage precision. Thread = (8-channel group, output pixel).
 __global__ void nchw_unfold_kernel(const float* __restrict__ in, View out, int dtype, int N, int C, int W, int kw, int sw,
                                    int pw) {
-  const int64_t total = (int64_t)N * out.H * out.W * out.C;
+  const int ohw = out.H * out.W;
+  const int npix = N * ohw, ng = out.C / 8;
+  const int total = npix * ng;
   const int64_t hw = (int64_t)out.H * W;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int ch = (int)(i % out.C);
-    const int64_t pix = i / out.C;
-    const int ow = (int)(pix % out.W);
-    const int64_t nh = pix / out.W;
-    const int h = (int)(nh % out.H);
-    const int64_t n = nh / out.H;
-    float x = 0.f;
-    if (ch < kw * C) {
-      const int j = ch / C, c = ch - (ch / C) * C;
-      const int w = ow * sw - pw + j;
-      if (w >= 0 && w < W) x = in[(n * C + c) * hw + (int64_t)h * W + w];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i / npix, pix = i - g * npix;
+    const int n = pix / ohw, rem = pix - n * ohw;
+    const int h = rem / out.W, ow = rem - h * out.W;
+    const float* row = in + (int64_t)n * C * hw + (int64_t)h * W;
+    const int w0 = ow * sw - pw;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ch = 8 * g + e;
+      v[e] = 0.f;
+      if (ch < kw * C) {
+        const int j = ch / C, c = ch - j * C;
+        const int w = w0 + j;
+        if (w >= 0 && w < W) v[e] = __ldg(row + (int64_t)c * hw + w);
+      }
     }
-    store_elem(out, dtype, pix, ch, x);
+    store8(out, dtype, pix, 8 * g, v);
   }
 }
 
+// (32-bit indices: the launcher checks N * C * H * W < 2^31)
 __global__ void nhwc_to_nchw_kernel(View in, int dtype, float* __restrict__ out, int N, int C) {
-  const int64_t hw = (int64_t)in.H * in.W;
-  const int64_t total = (int64_t)N * C * hw;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = i % hw;
-    const int64_t nc = i / hw;
-    const int c = (int)(nc % C);
-    const int64_t n = nc / C;
-    out[i] = load_elem(in, dtype, n * hw + p, c);
+  const int hw = in.H * in.W;
+  const int total = N * C * hw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int nc = i / hw, p = i - nc * hw;
+    const int n = nc / C, c = nc - n * C;
+    out[i] = load_elem(in, dtype, (int64_t)n * hw + p, c);
   }
 }
 
@@ -2439,27 +2501,34 @@ cudaError_t launch_stage(const StageDesc& sd, int dtype, int grid, cudaStream_t 
   return cudaErrorInvalidValue;
 }
 
+// the layout kernels store 8-channel vectors (16 B aligned) and index pixels in 32 bits
+static bool layout_ok(const View& v, int N) {
+  return v.C % 8 == 0 && v.cstride % 8 == 0 && v.coff % 8 == 0 && (v.ptr & 15) == 0 &&
+         (int64_t)N * v.H * v.W * (v.C / 8) < (int64_t)INT_MAX;
+}
+static int layout_grid(int64_t npix) {
+  const int64_t g = (npix + 255) / 256;
+  return (int)(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
+}
+
 cudaError_t launch_nchw_to_nhwc(const float* in, const View& out, int dtype, int N, int C, cudaStream_t st) {
-  const int64_t total = (int64_t)N * out.H * out.W * out.C;
-  int64_t g64 = (total + 255) / 256; int grid = (int)(g64 < 148 * 8 ? g64 : 148 * 8);
-  nchw_to_nhwc_kernel<<<grid, 256, 0, st>>>(in, out, dtype, N, C);
+  if (!layout_ok(out, N)) return cudaErrorInvalidValue;
+  nchw_to_nhwc_kernel<<<layout_grid((int64_t)N * out.H * out.W * (out.C / 8)), 256, 0, st>>>(in, out, dtype, N, C);
   return cudaGetLastError();
 }
 
 cudaError_t launch_nchw_unfold(const float* in, const View& out, int dtype, int N, int C, int W, int kw, int sw, int pw,
                                cudaStream_t st) {
-  const int64_t total = (int64_t)N * out.H * out.W * out.C;
-  int64_t g64 = (total + 255) / 256;
-  int grid = (int)(g64 < 148 * 8 ? g64 : 148 * 8);
-  nchw_unfold_kernel<<<grid, 256, 0, st>>>(in, out, dtype, N, C, W, kw, sw, pw);
+  if (!layout_ok(out, N)) return cudaErrorInvalidValue;
+  nchw_unfold_kernel<<<layout_grid((int64_t)N * out.H * out.W * (out.C / 8)), 256, 0, st>>>(in, out, dtype, N, C, W, kw,
+                                                                                            sw, pw);
   return cudaGetLastError();
 }
 
 cudaError_t launch_nhwc_to_nchw(const View& in, int dtype, float* out, int N, int C, cudaStream_t st) {
   const int64_t total = (int64_t)N * C * in.H * in.W;
-  int64_t g64 = (total + 255) / 256; int grid = (int)(g64 < 148 * 8 ? g64 : 148 * 8);
-  if (grid < 1) grid = 1;
-  nhwc_to_nchw_kernel<<<grid, 256, 0, st>>>(in, dtype, out, N, C);
+  if (total >= (int64_t)INT_MAX) return cudaErrorInvalidValue;
+  nhwc_to_nchw_kernel<<<layout_grid(total), 256, 0, st>>>(in, dtype, out, N, C);
   return cudaGetLastError();
 }
 
