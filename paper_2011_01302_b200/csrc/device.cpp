@@ -952,6 +952,7 @@ StagePlan* build_plan(Graph& g, int bpos, uint64_t mask, int strategy, int varia
       p.fd_howo = make_fastdiv((uint32_t)(p.Ho * p.Wo));
       p.fd_wo = make_fastdiv((uint32_t)p.Wo);
       p.fd_split = make_fastdiv((uint32_t)s.split);
+      p.fd_q4 = make_fastdiv((uint32_t)std::max(1, s.BN / 4));
       p.fd_ntn = make_fastdiv((uint32_t)s.ntn);
       p.fd_cin = make_fastdiv((uint32_t)in.C);
       p.fd_kw = make_fastdiv((uint32_t)p.kw);

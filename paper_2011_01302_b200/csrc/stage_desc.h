@@ -148,6 +148,7 @@ struct Problem {
   // reduction; with more (split / csplit global groups) the owners' csplit-summed rows go through the
   // global red.add + rendezvous path. 1 = no cluster reduction.
   int32_t csplit, csk_pad_;
+  FastDiv fd_q4;                    // split-K finalize: divisor BN / 4 (column quads per tile row)
 };
 
 // Kernel feature classes: the stage kernel is instantiated per class with only the code paths its

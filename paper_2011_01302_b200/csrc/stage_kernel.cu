@@ -1730,9 +1730,6 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const int n = tn0 + nn, oh = toh0 + i, ow = tow0 + rem - i * tWt;
         return (r < trows && n < nb && oh < Ho && ow < Wo) ? (n * Ho + oh) * Wo + ow : -1;
       };
-      const int m = pixel(etid);
-      const bool valid = m >= 0;
-      const int esz_out = P.dtype == ET_BF16 ? 2 : 4;
       const float* bias = reinterpret_cast<const float*>(P.bias);
       if (P.swap_ab) {
         // swap-AB tile: TMEM lane = output channel, columns = pixels. Each thread owns one channel;
@@ -2029,9 +2026,43 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const uint32_t stg = smem_u32(sepi) + (warp & 3) * 4096;
         constexpr int RPI = 32 / PPR;                       // rows per write-out instruction (4 / 8)
         int opix[32 / RPI];                                 // output pixel of each row this lane writes
+        if (!is_tt) {
 #pragma unroll
-        for (int it = 0; it < 32 / RPI; ++it) opix[it] = pixel((warp & 3) * 32 + it * RPI + lane / PPR);
+          for (int it = 0; it < 32 / RPI; ++it) opix[it] = pixel((warp & 3) * 32 + it * RPI + lane / PPR);
+        } else {
+          // patch tile: decode the lane's first row once, then step RPI rows (j, i, nn carry) instead
+          // of two divisions per row
+          const int r0 = (warp & 3) * 32 + lane / PPR;
+          int nn = fdiv(fthw, r0);
+          int rem = r0 - nn * thw;
+          int i = fdiv(ftw, rem), j = rem - i * tWt;
+          const int tRr = P.tR;
+#pragma unroll
+          for (int it = 0; it < 32 / RPI; ++it) {
+            const int r = r0 + it * RPI, n = tn0 + nn, oh = toh0 + i, ow = tow0 + j;
+            opix[it] = (r < trows && n < nb && oh < Ho && ow < Wo) ? (n * Ho + oh) * Wo + ow : -1;
+            j += RPI;
+            while (j >= tWt) {
+              j -= tWt;
+              if (++i == tRr) {
+                i = 0;
+                ++nn;
+              }
+            }
+          }
+        }
         const int sg0 = P.seg_begin, nsg = P.n_seg;
+        // one output segment (every conv but a merged one): its destination once per tile
+        char* s1_base = nullptr;
+        int s1_n0 = 0, s1_n1 = 0, s1_cs = 0, s1_relu = 0;
+        if (nsg == 1) {
+          const Segment& sg = segs[sg0];
+          s1_n0 = sg.n0;
+          s1_n1 = sg.n1;
+          s1_cs = sg.out.cstride;
+          s1_relu = sg.relu;
+          s1_base = reinterpret_cast<char*>(sg.out.ptr) + ((int64_t)sg.out.coff - sg.n0) * OESZ;
+        }
         for (int c0 = 0; c_owner && c0 < BNx; c0 += 32) {
           uint32_t va[16], vb[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
@@ -2072,12 +2103,20 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           char* dst = nullptr;
           int ocs = 0, relu = 0;
           // (columns past BN in the last round belong to the next N tile: never written from here)
-          for (int q = 0; q < nsg && c0 + p * (16 / OESZ) < BNx; ++q) {
-            const Segment& sg = segs[sg0 + q];
-            if (ncol >= sg.n0 && ncol < sg.n1) {
-              dst = reinterpret_cast<char*>(sg.out.ptr) + ((int64_t)sg.out.coff + ncol - sg.n0) * OESZ;
-              ocs = sg.out.cstride;
-              relu = sg.relu;
+          if (nsg == 1) {
+            if (c0 + p * (16 / OESZ) < BNx && ncol >= s1_n0 && ncol < s1_n1) {
+              dst = s1_base + (int64_t)ncol * OESZ;
+              ocs = s1_cs;
+              relu = s1_relu;
+            }
+          } else {
+            for (int q = 0; q < nsg && c0 + p * (16 / OESZ) < BNx; ++q) {
+              const Segment& sg = segs[sg0 + q];
+              if (ncol >= sg.n0 && ncol < sg.n1) {
+                dst = reinterpret_cast<char*>(sg.out.ptr) + ((int64_t)sg.out.coff + ncol - sg.n0) * OESZ;
+                ocs = sg.out.cstride;
+                relu = sg.relu;
+              }
             }
           }
           // coalesced write-out: lane -> (row, piece)
@@ -2179,6 +2218,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           // [s*trows/S, (s+1)*trows/S); all 128 threads, coalesced (consecutive threads sweep a
           // row's contiguous columns)
           const int bn = BNx, q4 = bn / 4;
+          const FastDiv fq4 = P.fd_q4;
           const int r0 = s * trows / P.split, r1 = (s + 1) * trows / P.split;
           const int total = (r1 - r0) * q4;
           // 4 elements x 4 slabs = 16 independent float4 loads in flight per thread
@@ -2188,7 +2228,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int idx = base + u * 128;
-              off[u] = idx < total ? (r0 + idx / q4) * bn + (idx % q4) * 4 : -1;
+              const int qr = fdiv(fq4, idx);   // (idx / q4 by multiply-shift: q4 = BN / 4)
+              off[u] = idx < total ? (r0 + qr) * bn + (idx - qr * q4) * 4 : -1;
               x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             const int nsl = slabs ? P.split : 1;
@@ -2212,7 +2253,8 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
             for (int u = 0; u < 4; ++u) {
               const int idx = base + u * 128;
               if (idx >= total) break;
-              const int r = r0 + idx / q4, col = (idx % q4) * 4;
+              const int qr = fdiv(fq4, idx);
+              const int r = r0 + qr, col = (idx - qr * q4) * 4;
               if (!slabs) stg_zero4_cg(tacc + off[u]);   // re-zero for the next launch
               const int ncol = nt * bn + col;
               const Segment* sgp = &segs[P.seg_begin];
