@@ -1789,21 +1789,33 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         const uint32_t tbase = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)acc * kMaxBN;
         const int out_tile = mt;
         if (P.split == 1) {
+          // 16 pixels per round: this thread's channel of each staged as [pixel][32 channels], one
+          // warp sync, then every lane stores pixels (lane / PPP) + k * (32 / PPP) of its piece
           for (int c0 = 0; c0 < BNx && c0 < Mx; c0 += 16) {
             uint32_t v[16];
             tmem_ld16(tbase + c0, v);
             tmem_ld_wait();
 #pragma unroll
-            for (int g4 = 0; g4 < 4; ++g4) {
-              if (c0 + 4 * g4 >= Mx) break;
-              float o[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                o[e] = __uint_as_float(v[4 * g4 + e]) + bv;
-                if (relu) o[e] = fmaxf(o[e], 0.f);
-              }
-              emit4(c0 + 4 * g4, o);
+            for (int e = 0; e < 16; ++e) {
+              float o = __uint_as_float(v[e]) + bv;
+              if (relu) o = fmaxf(o, 0.f);
+              if (DT == ET_BF16)
+                asm volatile("st.shared.b16 [%0], %1;" ::"r"(stg + (e * 32 + lane) * 2), "h"(bf16_bits(o)));
+              else
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(stg + (e * 32 + lane) * 4), "r"(__float_as_uint(rnd(o, DT))));
             }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 16 / (32 / PPP); ++k) {
+              const int px = sp + k * (32 / PPP);
+              if (qptr && c0 + px < Mx) {
+                uint32_t w0, w1, w2, w3;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                             : "r"(stg + px * 32 * OESZ + sq * 16));
+                stg_v4(qptr + (int64_t)(c0 + px) * qstride, w0, w1, w2, w3);
+              }
+            }
+            __syncwarp();
           }
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty[acc]));
@@ -2161,8 +2173,9 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // the splits of a tile reduce into the same lines: rotate the 32-column round and the 4-row
         // group order by split index so they do not queue on the same L2 lines at the same time
         const int nr32 = (BNx + 31) >> 5;
+        const int ks = s % nr32;   // (one division per tile, not per round)
         for (int k = 0; c_owner && k < nr32; ++k) {
-          const int c0 = ((k + s) % nr32) * 32, rot = s;
+          const int c0 = (k + ks < nr32 ? k + ks : k + ks - nr32) * 32, rot = s;
           uint32_t va[16], vb[16];
           acc_ld16<DT>(tbase + c0, sacc, c0, va);
           acc_ld16<DT>(tbase + c0 + 16, sacc, c0 + 16, vb);
@@ -2221,6 +2234,11 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           const FastDiv fq4 = P.fd_q4;
           const int r0 = s * trows / P.split, r1 = (s + 1) * trows / P.split;
           const int total = (r1 - r0) * q4;
+          // one output segment (every conv but a merged one): destination fields once per tile
+          const bool seg1 = P.n_seg == 1;
+          const Segment& sg1 = segs[P.seg_begin];
+          const int f1_n0 = sg1.n0, f1_n1 = sg1.n1, f1_cs = sg1.out.cstride, f1_relu = sg1.relu;
+          char* const f1_base = reinterpret_cast<char*>(sg1.out.ptr) + ((int64_t)sg1.out.coff - sg1.n0) * (DT == ET_BF16 ? 2 : 4);
           // 4 elements x 4 slabs = 16 independent float4 loads in flight per thread
           for (int base = etid; base < total; base += 128 * 4) {
             float4 x[4];
@@ -2257,32 +2275,37 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               const int r = r0 + qr, col = (idx - qr * q4) * 4;
               if (!slabs) stg_zero4_cg(tacc + off[u]);   // re-zero for the next launch
               const int ncol = nt * bn + col;
-              const Segment* sgp = &segs[P.seg_begin];
-              if (P.n_seg > 1) {
-                for (int q = 0; q < P.n_seg; ++q)
-                  if (ncol >= segs[P.seg_begin + q].n0 && ncol < segs[P.seg_begin + q].n1) {
-                    sgp = &segs[P.seg_begin + q];
+              int n0 = f1_n0, n1 = f1_n1, ocs = f1_cs, relu = f1_relu;
+              char* obase = f1_base;
+              if (!seg1) {
+                for (int q = 0; q < P.n_seg; ++q) {
+                  const Segment& sg = segs[P.seg_begin + q];
+                  if (ncol >= sg.n0 && ncol < sg.n1) {
+                    n0 = sg.n0;
+                    n1 = sg.n1;
+                    ocs = sg.out.cstride;
+                    relu = sg.relu;
+                    obase = reinterpret_cast<char*>(sg.out.ptr) + ((int64_t)sg.out.coff - sg.n0) * (DT == ET_BF16 ? 2 : 4);
                     break;
                   }
+                }
               }
-              if (ncol < sgp->n0 || ncol >= sgp->n1) continue;
+              if (ncol < n0 || ncol >= n1) continue;
               const int px = pixel(r);
               if (px < 0) continue;
               float o[4] = {x[u].x + sbias[col], x[u].y + sbias[col + 1], x[u].z + sbias[col + 2], x[u].w + sbias[col + 3]};
-              if (sgp->relu) {
+              if (relu) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) o[e] = fmaxf(o[e], 0.f);
               }
-              const int64_t pix = px;
+              const int64_t eoff = (int64_t)px * ocs + ncol;   // elements from obase
               if (DT == ET_BF16) {
                 __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
-                stg_v2(reinterpret_cast<__nv_bfloat16*>(sgp->out.ptr) + pix * sgp->out.cstride + sgp->out.coff + ncol -
-                           sgp->n0,
-                       *reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+                stg_v2(reinterpret_cast<__nv_bfloat16*>(obase) + eoff, *reinterpret_cast<uint32_t*>(&h0),
+                       *reinterpret_cast<uint32_t*>(&h1));
               } else {
-                stg_v4(reinterpret_cast<float*>(sgp->out.ptr) + pix * sgp->out.cstride + sgp->out.coff + ncol - sgp->n0,
-                       __float_as_uint(rnd(o[0], DT)), __float_as_uint(rnd(o[1], DT)), __float_as_uint(rnd(o[2], DT)),
-                       __float_as_uint(rnd(o[3], DT)));
+                stg_v4(reinterpret_cast<float*>(obase) + eoff, __float_as_uint(rnd(o[0], DT)), __float_as_uint(rnd(o[1], DT)),
+                       __float_as_uint(rnd(o[2], DT)), __float_as_uint(rnd(o[3], DT)));
               }
             }
           }
