@@ -1449,25 +1449,38 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #ifdef IOS_TRACE_FINE
           if (lane == 0 && tfirst) IOS_TRACE(15);   // TMA geometry ready
 #endif
+          // tap-TMA chunk c = (tap (ti, tj), channel block cb): decoded once for c0, then stepped
+          const bool is_tt = P.tt != 0;
+          int cb = 0, ti = 0, tj = 0;
+          if (is_tt) {
+            const int tap = fdiv(P.fd_kblk, c0);
+            cb = c0 - tap * kblk;
+            ti = fdiv(P.fd_kw, tap);
+            tj = tap - ti * kwid;
+          }
+          const uint8_t* wsrc_c = wsrc + c0 * wstep;
           for (int c = c0; c < c1; ++c) {
             mbar_wait(smem_u32(&empty[ring.slot]), ring.phase ^ 1u);
             if (lane == 0) {
               const uint32_t fb = smem_u32(&full[ring.slot]);
               mbar_arrive_expect_tx(fb, xbytes + bbytes);
               if (tfirst && c == c0) IOS_TRACE(9);
-              if (P.tt) {
-                const int tap = fdiv(P.fd_kblk, c);
-                const int cb = c - tap * kblk;
-                const int ti = fdiv(P.fd_kw, tap);
-                const int tj = tap - ti * kwid;
+              if (is_tt)
                 tma_load_4d(smem_u32(slotA(ring.slot) + xoff), tmap, cb * ELEMS, iw0 + tj, ih0 + ti, tn0, fb);
-              } else {
+              else
                 tma_load_2d(smem_u32(slotA(ring.slot) + xoff), tmap, c * ELEMS, xrow0, fb);
-              }
               if (tfirst && c == c0) IOS_TRACE(10);
-              bulk_g2s(smem_u32(slotA(ring.slot) + woff), wsrc + c * wstep, bbytes, fb);
+              bulk_g2s(smem_u32(slotA(ring.slot) + woff), wsrc_c, bbytes, fb);
               mbar_arrive_cnt(fb, kProducerWarps);   // stands in for the 4 producer warps' arrivals
               if (tfirst && c - c0 < 2) IOS_TRACE(c == c0 ? 2 : 12);
+            }
+            wsrc_c += wstep;
+            if (++cb == kblk) {
+              cb = 0;
+              if (++tj == kwid) {
+                tj = 0;
+                ++ti;
+              }
             }
             __syncwarp();
             ring.next();

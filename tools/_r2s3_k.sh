@@ -4,5 +4,5 @@ for r in 1 2 3; do for v in head cur; do
   if [ $v = cur ]; then L=""; else L=paper_2011_01302_b200/build/libios_$v.so; fi
   echo -n "$v "; IOS_LIB=$L timeout 200 python tools/time_schedule.py profiles/r2_sched_inception.json --steps 100 2>&1 | tail -1
   echo -n "$v "; IOS_LIB=$L timeout 200 python tools/seq_greedy.py --net inception_v3 --steps 50 2>&1 | tail -1
-  echo -n "$v "; IOS_LIB=$L timeout 200 python tools/seq_greedy.py --net nasnet_a_large --steps 20 2>&1 | tail -1
+  echo -n "$v "; IOS_LIB=$L timeout 200 python tools/seq_greedy.py --net squeezenet --batch 128 --steps 20 2>&1 | tail -1
 done; done
