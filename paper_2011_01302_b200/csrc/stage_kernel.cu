@@ -1659,11 +1659,14 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           const uint32_t b0 = smem_u32(slotB(ring.slot));
           __syncwarp();
           if (elect_one()) {
+            // descriptor of the chunk's first 32 B of K; each next 32 B step moves the start address
+            // field (address >> 4) by 2 (128 B-swizzled rows) or 16 (core-matrix layout, 256 B)
+            const uint64_t ad = a_sw128 ? umma_desc_sw128(a0) : umma_desc(a0, 128, 1024);
+            const uint64_t bd = b_sw128 ? umma_desc_sw128(b0) : umma_desc(b0, 128, 1024);
+            const uint32_t astep = a_sw128 ? 2u : 16u, bstep = b_sw128 ? 2u : 16u;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)   // 4 x 32 B of K per 128 B chunk
-              umma<DT>(tmem_d, a_sw128 ? umma_desc_sw128(a0 + kk * 32) : umma_desc(a0 + kk * 256, 128, 1024),
-                       b_sw128 ? umma_desc_sw128(b0 + kk * 32) : umma_desc(b0 + kk * 256, 128, 1024), idesc,
-                       (c > c0 || kk > 0) ? 1u : 0u);
+              umma<DT>(tmem_d, ad + kk * astep, bd + kk * bstep, idesc, (c > c0 || kk > 0) ? 1u : 0u);
             umma_commit(smem_u32(&empty[ring.slot]));
           }
           __syncwarp();
@@ -2100,8 +2103,17 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(e < 16 ? va[e] : vb[e - 16]);
           if (kCsk && cD > 1) add_received(c0, o);
+          {
+            const float4* sb4 = reinterpret_cast<const float4*>(sbias + c0);   // 16 B aligned
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] += sbias[c0 + e];
+            for (int e4 = 0; e4 < 8; ++e4) {
+              const float4 b4 = sb4[e4];
+              o[4 * e4] += b4.x;
+              o[4 * e4 + 1] += b4.y;
+              o[4 * e4 + 2] += b4.z;
+              o[4 * e4 + 3] += b4.w;
+            }
+          }
 #pragma unroll
           for (int p = 0; p < PPR; ++p) {
             uint32_t w[4];
