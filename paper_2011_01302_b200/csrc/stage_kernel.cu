@@ -2198,7 +2198,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
         // the splits of a tile reduce into the same lines: rotate the 32-column round and the 4-row
         // group order by split index so they do not queue on the same L2 lines at the same time
         const int nr32 = (BNx + 31) >> 5;
-        const int ks = s % nr32;   // (one division per tile, not per round)
+        const int ks = nr32 == 1 ? 0 : (int)((uint32_t)s % (uint32_t)nr32);   // (once per tile, not per round)
         for (int k = 0; c_owner && k < nr32; ++k) {
           const int c0 = (k + ks < nr32 ? k + ks : k + ks - nr32) * 32, rot = s;
           uint32_t va[16], vb[16];
@@ -2257,7 +2257,7 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
           // row's contiguous columns)
           const int bn = BNx, q4 = bn / 4;
           const FastDiv fq4 = P.fd_q4;
-          const int r0 = s * trows / P.split, r1 = (s + 1) * trows / P.split;
+          const int r0 = fdiv(P.fd_split, s * trows), r1 = fdiv(P.fd_split, (s + 1) * trows);   // s*trows/S
           const int total = (r1 - r0) * q4;
           // one output segment (every conv but a merged one): destination fields once per tile
           const bool seg1 = P.n_seg == 1;
@@ -2275,7 +2275,12 @@ __global__ void __launch_bounds__(kThreads, 1) ios_stage_kernel(const StageDesc 
               off[u] = idx < total ? (r0 + qr) * bn + (idx - qr * q4) * 4 : -1;
               x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            const int nsl = slabs ? P.split : 1;
+            const int nsl = slabs ? P.split : 0;
+            if (!slabs) {   // one reduced slab: 4 independent loads
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (off[u] >= 0) x[u] = __ldcg(reinterpret_cast<const float4*>(tacc + off[u]));
+            }
             for (int j0 = 0; j0 < nsl; j0 += 4) {
               float4 t[4][4];
 #pragma unroll
